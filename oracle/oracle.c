@@ -1,0 +1,291 @@
+/*
+ * oracle/oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, single-threaded CPU reference for the GraphPy sparse hot path
+ * (arxiv 2402.03548).  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no
+ * code with the CUDA path (paper_2402_03548_b200/) and never reads anything the
+ * CUDA path produced.
+ *
+ * Every float result is accumulated in fp64 from the fp32 inputs (exact in
+ * fp64); alongside each value the oracle returns T = sum of |terms| so the
+ * tests can apply the acceptance bound |gpu - oracle| <= 1e-5 (T + 1)
+ * (BASELINE.json north_star).  The method is exact (it reaches the plain
+ * definitions), so each function is the definition written out; there is no
+ * blocking, fusion or reordering.
+ *
+ * Notation (SURVEY.md §8 / DESIGN.md): an input edge i is (src[i] -> dst[i]),
+ * i.e. A[dst][src] = 1.  The "fwd" structure groups edges by destination
+ * (CSR rows, §Background), the "rev" structure groups them by
+ * source (CSC / transpose, P:1318, P:1497-1498 SYS-P2).
+ *
+ * Pins: tests/test_oracle.py (hand examples SPEC S:80-82, S:152-155, S:196-198;
+ * closed form D^-1/2 A D^-1/2 X on dense adjacency; brute-force dense
+ * products on <=64 vertices; adjoint / bilinear identities; softmax
+ * characterisation).  Parity pinned for every function below.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+enum { OR_NORM_NONE = 0, OR_NORM_RIGHT = 1, OR_NORM_BOTH = 2 };
+
+/* ------------------------------------------------------------------ C1 --- */
+/* Graph build, §Storage Format ("COO ... arranged in CSR-style",
+ * "CSR and COO ... allocated consecutive edge IDs", "CSC requires an explicit
+ * edge ID array") and DESIGN.md readings L5/L6/L7:
+ *   order  = positions i sorted by (dst[i], src[i], i)       (ties: input order)
+ *   fwd_off[v] = #{i : dst[i] < v};  fwd_col[j] = src[order[j]];
+ *   coo_to_eid[order[j]] = j          (the edge ID of fwd slot j is j)
+ *   rorder = slots j sorted by (src_j, dst_j, j)
+ *   rev_off[u] = #{j : src_j < u};  rev_col[k] = dst_{rorder[k]};  rev_eid[k] = rorder[k]
+ */
+typedef struct { int64_t k1, k2, idx; } key3;
+
+static int cmp_key3(const void *a, const void *b) {
+    const key3 *x = (const key3 *)a, *y = (const key3 *)b;
+    if (x->k1 != y->k1) return x->k1 < y->k1 ? -1 : 1;
+    if (x->k2 != y->k2) return x->k2 < y->k2 ? -1 : 1;
+    if (x->idx != y->idx) return x->idx < y->idx ? -1 : 1;
+    return 0;
+}
+
+/* returns 0 ok, -1 bad vertex id, -2 out of memory */
+int oracle_build(int64_t V, int64_t E, const int64_t *src, const int64_t *dst,
+                 int64_t *fwd_off, int32_t *fwd_col, int64_t *rev_off, int32_t *rev_col,
+                 int32_t *rev_eid, int32_t *coo_to_eid) {
+    for (int64_t i = 0; i < E; i++)
+        if (src[i] < 0 || src[i] >= V || dst[i] < 0 || dst[i] >= V) return -1;
+    key3 *a = (key3 *)malloc(sizeof(key3) * (size_t)(E > 0 ? E : 1));
+    int64_t *cnt = (int64_t *)calloc((size_t)V + 1, sizeof(int64_t));
+    if (!a || !cnt) { free(a); free(cnt); return -2; }
+
+    /* fwd: sort positions by (dst, src, position) */
+    for (int64_t i = 0; i < E; i++) { a[i].k1 = dst[i]; a[i].k2 = src[i]; a[i].idx = i; }
+    qsort(a, (size_t)E, sizeof(key3), cmp_key3);
+    for (int64_t i = 0; i < E; i++) cnt[dst[i] + 1]++;         /* fwd_off[v] = #{i: dst[i] < v} */
+    fwd_off[0] = 0;
+    for (int64_t v = 0; v < V; v++) fwd_off[v + 1] = fwd_off[v] + cnt[v + 1];
+    for (int64_t j = 0; j < E; j++) {
+        fwd_col[j] = (int32_t)src[a[j].idx];
+        coo_to_eid[a[j].idx] = (int32_t)j;
+    }
+    /* rev: sort fwd slots j by (src_j, dst_j, j); dst_j = dst[order[j]] */
+    for (int64_t j = 0; j < E; j++) { a[j].k1 = src[a[j].idx]; a[j].k2 = dst[a[j].idx]; a[j].idx = j; }
+    qsort(a, (size_t)E, sizeof(key3), cmp_key3);
+    memset(cnt, 0, sizeof(int64_t) * ((size_t)V + 1));
+    for (int64_t i = 0; i < E; i++) cnt[src[i] + 1]++;         /* rev_off[u] = #{j: src_j < u} */
+    rev_off[0] = 0;
+    for (int64_t u = 0; u < V; u++) rev_off[u + 1] = rev_off[u] + cnt[u + 1];
+    for (int64_t k = 0; k < E; k++) {
+        rev_col[k] = (int32_t)a[k].k2;
+        rev_eid[k] = (int32_t)a[k].idx;
+    }
+    free(a); free(cnt);
+    return 0;
+}
+
+/* ---------------------------------------------------------------- C2/C3 --- */
+/* Degrees with the clamp d^ = max(d,1) (§Requirement Mismatch, "sets
+ * the degree to 1.0").  d_in(v) = fwd row length, d_out(u) = rev
+ * row length (L2).  Scales per DESIGN.md L1 / SURVEY §8(c) C3:
+ *   NONE : s_dst = 1,              s_src = 1
+ *   RIGHT: s_dst = 1/d^_in(v),     s_src = 1          (D_in^-1 A)
+ *   BOTH : s_dst = d^_in(v)^-1/2,  s_src = d^_out(u)^-1/2   (D^-1/2 A D^-1/2, BJ) */
+static double clamp_deg(int64_t d) { return d < 1 ? 1.0 : (double)d; }
+static double s_dst(int norm, const int64_t *fwd_off, int64_t v) {
+    double d = clamp_deg(fwd_off[v + 1] - fwd_off[v]);
+    if (norm == OR_NORM_RIGHT) return 1.0 / d;
+    if (norm == OR_NORM_BOTH) return 1.0 / sqrt(d);
+    return 1.0;
+}
+static double s_src(int norm, const int64_t *rev_off, int64_t u) {
+    double d = clamp_deg(rev_off[u + 1] - rev_off[u]);
+    if (norm == OR_NORM_BOTH) return 1.0 / sqrt(d);
+    return 1.0;
+}
+
+/* Degree scales as arrays (tests check C2/C3 against the SPEC degrees). */
+void oracle_scales(int64_t V, const int64_t *fwd_off, const int64_t *rev_off, int norm,
+                   double *sdst, double *ssrc) {
+    for (int64_t v = 0; v < V; v++) {
+        sdst[v] = s_dst(norm, fwd_off, v);
+        ssrc[v] = s_src(norm, rev_off, v);
+    }
+}
+
+/* ------------------------------------------------------------------ C4 --- */
+/* gSpMMv with fused degree normalisation (Table 1; P:607-612;
+ * P:2024-2027 §Kernel Design "gSpMMv^T"; P:1333-1335 Class B):
+ *   fwd: out[v,f] = s_dst(v) * sum_{j in fwd row v} s_src(fwd_col[j]) * X[fwd_col[j], f]
+ *   rev: out[u,f] = s_src(u) * sum_{k in rev row u} s_dst(rev_col[k]) * X[rev_col[k], f]
+ * (rev is the exact adjoint of fwd; "Backward Computation",
+ *  P:1536-1540 SYS-P3: the column-side scale is applied per non-zero).
+ * T[v,f] = row scale * sum |col scale * X|.
+ * sel: NULL -> all V rows (out has V rows); else the nsel listed rows in order. */
+int oracle_gspmm(int64_t V, const int64_t *fwd_off, const int32_t *fwd_col,
+                 const int64_t *rev_off, const int32_t *rev_col,
+                 const float *X, int64_t F, int64_t ldx, int norm, int reverse,
+                 int64_t nsel, const int64_t *sel, double *out, double *T) {
+    int64_t n = sel ? nsel : V;
+    for (int64_t r = 0; r < n; r++) {
+        int64_t v = sel ? sel[r] : r;
+        if (v < 0 || v >= V) return -1;
+        const int64_t *off = reverse ? rev_off : fwd_off;
+        const int32_t *col = reverse ? rev_col : fwd_col;
+        double rs = reverse ? s_src(norm, rev_off, v) : s_dst(norm, fwd_off, v);
+        for (int64_t f = 0; f < F; f++) {
+            double acc = 0.0, tacc = 0.0;
+            for (int64_t j = off[v]; j < off[v + 1]; j++) {
+                int64_t u = col[j];
+                double cs = reverse ? s_dst(norm, fwd_off, u) : s_src(norm, rev_off, u);
+                double term = cs * (double)X[u * ldx + f];
+                acc += term;
+                tacc += fabs(term);
+            }
+            out[r * F + f] = rs * acc;
+            if (T) T[r * F + f] = rs * tacc;
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ C5 --- */
+/* Weighted gSpMM, multi-head (gSpMMve P:1329, "vector feature for
+ * each edge"; its transpose gSpMMve^T fetches the edge value through the edge
+ * ID, §Kernel Design, P:564 gSpMMveid).  Head layout (DESIGN.md
+ * L10): vertex tensors [V, H*Fh], head h = columns [h*Fh, (h+1)*Fh); edge
+ * tensor w [E, H] indexed by edge ID.
+ *   fwd: out[v, h*Fh+f] = sum_{j in fwd row v} w[j, h] * X[fwd_col[j], h*Fh+f]
+ *   rev: out[u, h*Fh+f] = sum_{k in rev row u} w[rev_eid[k], h] * X[rev_col[k], h*Fh+f]
+ * T = sum |w * X|. */
+int oracle_gspmm_weighted(int64_t V, const int64_t *fwd_off, const int32_t *fwd_col,
+                          const int64_t *rev_off, const int32_t *rev_col, const int32_t *rev_eid,
+                          const float *X, int64_t F, int64_t ldx, const float *w, int64_t H,
+                          int reverse, int64_t nsel, const int64_t *sel, double *out, double *T) {
+    if (H <= 0 || F % H != 0) return -2;
+    int64_t Fh = F / H, n = sel ? nsel : V;
+    for (int64_t r = 0; r < n; r++) {
+        int64_t v = sel ? sel[r] : r;
+        if (v < 0 || v >= V) return -1;
+        for (int64_t c = 0; c < F; c++) {
+            int64_t h = c / Fh;
+            double acc = 0.0, tacc = 0.0;
+            if (!reverse) {
+                for (int64_t j = fwd_off[v]; j < fwd_off[v + 1]; j++) {
+                    double term = (double)w[j * H + h] * (double)X[(int64_t)fwd_col[j] * ldx + c];
+                    acc += term; tacc += fabs(term);
+                }
+            } else {
+                for (int64_t k = rev_off[v]; k < rev_off[v + 1]; k++) {
+                    double term = (double)w[(int64_t)rev_eid[k] * H + h] * (double)X[(int64_t)rev_col[k] * ldx + c];
+                    acc += term; tacc += fabs(term);
+                }
+            }
+            out[r * F + c] = acc;
+            if (T) T[r * F + c] = tacc;
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ C6 --- */
+/* gSDDMMvv (Table 1; "the vertex-level features of row ID and
+ * column ID of each non-zero element ... perform dot product"):
+ * X is indexed by the row (destination), Y by the column (source) (L8):
+ *   out[j, h] = sum_{f < Fh} X[v, h*Fh+f] * Y[fwd_col[j], h*Fh+f]   for slot j of row v.
+ * Output is indexed by edge ID (= fwd slot).  With sel, the edges of the
+ * selected rows are packed row after row (each row's slots in order). */
+int oracle_gsddmm(int64_t V, const int64_t *fwd_off, const int32_t *fwd_col,
+                  const float *X, int64_t ldx, const float *Y, int64_t ldy, int64_t F, int64_t H,
+                  int64_t nsel, const int64_t *sel, double *out, double *T) {
+    if (H <= 0 || F % H != 0) return -2;
+    int64_t Fh = F / H, n = sel ? nsel : V, o = 0;
+    for (int64_t r = 0; r < n; r++) {
+        int64_t v = sel ? sel[r] : r;
+        if (v < 0 || v >= V) return -1;
+        for (int64_t j = fwd_off[v]; j < fwd_off[v + 1]; j++, o++) {
+            int64_t u = fwd_col[j];
+            for (int64_t h = 0; h < H; h++) {
+                double acc = 0.0, tacc = 0.0;
+                for (int64_t f = 0; f < Fh; f++) {
+                    double term = (double)X[v * ldx + h * Fh + f] * (double)Y[u * ldy + h * Fh + f];
+                    acc += term; tacc += fabs(term);
+                }
+                out[o * H + h] = acc;
+                if (T) T[o * H + h] = tacc;
+            }
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ C7 --- */
+/* Edge softmax grouped by destination (fwd row) -- part of GAT's layer
+ * (P:197), composite defined in SPEC S:217-225 and DESIGN.md L9:
+ *   m = max_j e[j,h];  S = sum_j exp(e[j,h] - m);  out[j,h] = exp(e[j,h] - m) / S
+ * over the slots j of row v.  Empty rows produce nothing. */
+int oracle_edge_softmax(int64_t V, const int64_t *fwd_off, const float *e, int64_t H,
+                        int64_t nsel, const int64_t *sel, double *out) {
+    int64_t n = sel ? nsel : V, o = 0;
+    for (int64_t r = 0; r < n; r++) {
+        int64_t v = sel ? sel[r] : r;
+        if (v < 0 || v >= V) return -1;
+        int64_t b = fwd_off[v], en = fwd_off[v + 1];
+        for (int64_t h = 0; h < H; h++) {
+            double m = -INFINITY;
+            for (int64_t j = b; j < en; j++) if ((double)e[j * H + h] > m) m = (double)e[j * H + h];
+            double S = 0.0;
+            for (int64_t j = b; j < en; j++) S += exp((double)e[j * H + h] - m);
+            for (int64_t j = b; j < en; j++) out[(o + (j - b)) * H + h] = exp((double)e[j * H + h] - m) / S;
+        }
+        o += en - b;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ C8 --- */
+/* Edge-balanced contiguous row partition (BJ north_star
+ * "destination-row partitioner"):  b_0 = 0, b_P = V,
+ *   b_p = min { v : off[v] >= ceil(p * E / P) }   for 0 < p < P. */
+int oracle_partition_bounds(int64_t V, const int64_t *off, int64_t nparts, int64_t *bounds) {
+    if (nparts < 1) return -2;
+    int64_t E = off[V];
+    bounds[0] = 0;
+    for (int64_t p = 1; p < nparts; p++) {
+        /* ceil(p*E/P) in exact integer arithmetic */
+        __int128 num = (__int128)p * E;
+        int64_t target = (int64_t)((num + nparts - 1) / nparts);
+        int64_t v = 0;
+        while (v < V && off[v] < target) v++;
+        bounds[p] = v;
+    }
+    bounds[nparts] = V;
+    return 0;
+}
+
+/* The partition's structure in the padded rank-major layout (DESIGN.md
+ * "Multi-GPU"): R = max_p (b_{p+1} - b_p); partition `part` owns rows
+ * [b_part, b_part+1); local row r has the edges of global row b_part + r, in
+ * the same order; every column id v is remapped to p(v)*R + (v - b_{p(v)}),
+ * where p(v) is the part holding v.  Rows [nrows_local, R) are empty.
+ * loc_off has R+1 entries, loc_col has off[b_{part+1}] - off[b_part]. */
+int oracle_partition_structure(int64_t V, const int64_t *off, const int32_t *col,
+                               int64_t nparts, const int64_t *bounds, int64_t part,
+                               int64_t *loc_off, int32_t *loc_col) {
+    int64_t R = 0;
+    for (int64_t p = 0; p < nparts; p++)
+        if (bounds[p + 1] - bounds[p] > R) R = bounds[p + 1] - bounds[p];
+    int64_t b = bounds[part], e = bounds[part + 1], base = off[b];
+    for (int64_t r = 0; r <= R; r++) {
+        int64_t g = b + r < e ? b + r : e;
+        loc_off[r] = off[g] - base;
+    }
+    for (int64_t j = off[b]; j < off[e]; j++) {
+        int64_t v = col[j], p = 0;
+        while (!(bounds[p] <= v && v < bounds[p + 1])) p++;
+        loc_col[j - base] = (int32_t)(p * R + (v - bounds[p]));
+    }
+    return 0;
+}
