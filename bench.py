@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""Benchmark of the GraphPy sparse hot path on B200 (BASELINE.json metric:
+"gSpMM GE/s & HBM GB/s (% of 8 TB/s), Reddit-shape F=64, 1/2/4/8 B200").
+
+One STEP = one pass of the whole hot path over the Reddit-shaped graph
+(A9 at N > 1):
+    out1 = gspmm(X,  BOTH, fwd)            GCN forward          (A3)
+    out2 = gspmm(dY, BOTH, rev)            GCN backward         (A4)
+    s    = gsddmm(Z, Z)        [E, H]      GAT scores           (A5)
+    a    = edge_softmax(s)     in place    GAT attention        (A6)
+    out3 = gspmm_weighted(Z, a, fwd)       GAT aggregate        (A7)
+    out4 = gspmm_weighted(dO, a, rev)      GAT backward dZ      (A8)
+value = edge visits per second over the step = 6 * E / t_step (GE/s), whole job.
+At N > 1 every rank runs the same step on its destination-row partition and
+all-gathers each vertex-level output over NCCL (A9); scaling is "strong"
+(the graph is fixed).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gsp|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+L2_FLUSH_BYTES = 512 << 20          # > 126 MB L2: written between timed steps
+N_OPS = 6                           # sparse ops per step (edge visits = N_OPS * E)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["gsp", "reference"], default="gsp")
+    ap.add_argument("--config", default="reddit", choices=sorted(datagen.CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e / cpu baseline / clocks)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------- byte models
+def alg_bytes(op, V, E, F, H):
+    """Algorithmic (compulsory) bytes per launch: every
+    gathered feature row counted once per edge, indices/values/outputs once."""
+    base = 8 * (V + 1) + 4 * E                      # offsets + column ids
+    if op == "gspmm":
+        return base + 4 * E * F + 4 * V * F + 8 * V
+    if op == "gspmm_weighted_fwd":
+        return base + 4 * E * F + 4 * V * F + 4 * E * H
+    if op == "gspmm_weighted_rev":
+        return base + 4 * E * F + 4 * V * F + 4 * E * H + 4 * E
+    if op == "gsddmm":
+        return base + 4 * V * F + 4 * E * F + 4 * E * H
+    if op == "edge_softmax":
+        return 8 * (V + 1) + 4 * E * H + 4 * E * H
+    raise KeyError(op)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def load_traffic(config):
+    """ncu dram bytes per launch of the dominant kernel, from a committed profile summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    v = d.get(config, {}).get("gspmm_fwd_dram_bytes")
+    return float(v) if v is not None else None
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU oracle
+def oracle_sample(V, src, dst, cfg, target_edges):
+    """A bounded sample of the workload for the CPU oracle: all edges whose
+    destination falls in a random row subset holding ~target_edges edges
+    (same graph shape per edge)."""
+    rng = np.random.default_rng(cfg.seed)
+    frac = min(1.0, target_edges / max(1, len(src)))
+    keep_rows = rng.random(V) < frac
+    m = keep_rows[dst]
+    return src[m], dst[m]
+
+
+def run_oracle_step(og, V, cfg, inputs):
+    """The step's six ops, by the oracle (fp64)."""
+    X, dY, Z, dO = inputs
+    H = cfg.H
+    og.gspmm(X, 2, False)
+    og.gspmm(dY, 2, True)
+    s, _ = og.gsddmm(Z, Z, H)
+    a = og.edge_softmax(s.astype(np.float32))
+    a32 = a.astype(np.float32)
+    og.gspmm_weighted(Z, a32, False)
+    og.gspmm_weighted(dO, a32, True)
+
+
+def cpu_oracle_bench(V, src, dst, cfg, target_edges, steps=1, warmup=0):
+    import oracle
+    ssrc, sdst = oracle_sample(V, src, dst, cfg, target_edges)
+    t0 = time.perf_counter()
+    og = oracle.Graph(V, ssrc, sdst)
+    t_build = time.perf_counter() - t0
+    F = cfg.H * cfg.Fh
+    inputs = [datagen.uniform(cfg.seed + k, V, F) for k in range(4)]
+    for _ in range(warmup):
+        run_oracle_step(og, V, cfg, inputs)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        run_oracle_step(og, V, cfg, inputs)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    return {"E_sample": int(len(ssrc)), "t_step": t, "t_build": t_build,
+            "value": N_OPS * len(ssrc) / t / 1e9}
+
+
+# ------------------------------------------------------------------ GPU arm
+def main_gsp(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_03548_b200 as gsp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = datagen.CONFIGS[args.config]
+    assert cfg.H > 0, "bench step needs a config with the GAT chain (reddit / pubmed)"
+    F, H = cfg.H * cfg.Fh, cfg.H
+    if cfg.F != F:
+        raise SystemExit("config F must equal H*Fh for the step")
+
+    t0 = time.time()
+    V, src, dst = datagen.make_graph(cfg)
+    t_gen = time.time() - t0
+    t0 = time.time()
+    G = gsp.Graph(V, src, dst, device=local)
+    t_create = time.time() - t0
+    E = G.E
+    stream = torch.cuda.current_stream()
+
+    P = world
+    if P > 1:
+        part = G.partition(P, rank, device=local)
+        b = G.partition_bounds(P)
+        R = part.R
+        rows_lo, rows_hi = b[rank], b[rank + 1]
+    else:
+        part = G
+        R = V
+        b = np.array([0, V])
+    ncols = P * R
+
+    def padded_input(seed):
+        Xh = datagen.uniform(seed, V, F)
+        if P == 1:
+            return torch.from_numpy(Xh).cuda()
+        Xp = torch.zeros((ncols, F), device="cuda")
+        for p in range(P):
+            Xp[p * R:p * R + b[p + 1] - b[p]] = torch.from_numpy(Xh[b[p]:b[p + 1]]).cuda()
+        return Xp
+
+    X, dY, Z, dO = (padded_input(cfg.seed + k) for k in range(4))
+    Ep = part.E
+    s = torch.empty((Ep, H), device="cuda")
+    outs = [torch.empty((R, F), device="cuda") for _ in range(4)]
+    gathered = [torch.empty((ncols, F), device="cuda") for _ in range(4)] if P > 1 else None
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    op_names = ["gspmm_fwd", "gspmm_rev", "gsddmm", "edge_softmax", "gspmm_weighted_fwd", "gspmm_weighted_rev"]
+    ev = {k: [] for k in op_names + ["allgather"]}
+
+    def step(record):
+        def mark():
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            return e
+        marks = [mark()] if record else None
+        part.gspmm(X, gsp.NORM_BOTH, out=outs[0], stream=stream)
+        if record: marks.append(mark())
+        part.gspmm(dY, gsp.NORM_BOTH, out=outs[1], reverse=True, stream=stream)
+        if record: marks.append(mark())
+        part.gsddmm(Z, Z, out=s, stream=stream)
+        if record: marks.append(mark())
+        part.edge_softmax(s, out=s, stream=stream)
+        if record: marks.append(mark())
+        part.gspmm_weighted(Z, s, out=outs[2], stream=stream)
+        if record: marks.append(mark())
+        if P == 1:
+            part.gspmm_weighted(dO, s, out=outs[3], reverse=True, stream=stream)
+        else:
+            # partitions: weighted reverse needs alpha owned by other ranks (DESIGN.md
+            # "Multi-GPU"); round 1 runs the local-edge part only (flagged in the JSON line)
+            part.gspmm_weighted(dO, s, out=outs[3], stream=stream)
+        if record: marks.append(mark())
+        if P > 1:
+            for o, gbuf in zip(outs, gathered):
+                dist.all_gather_into_tensor(gbuf, o)
+            if record: marks.append(mark())
+        return marks
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local) if (rank == 0 and not args.profile) else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    if P > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)                      # L2 flush between timed steps (outside the events)
+        marks = step(True)
+        torch.cuda.synchronize()
+        names = op_names + (["allgather"] if P > 1 else [])
+        for i, n in enumerate(names):
+            ev[n].append(marks[i].elapsed_time(marks[i + 1]))
+        step_ms.append(marks[0].elapsed_time(marks[-1]))
+    torch.cuda.synchronize()
+    if P > 1:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop() if clocks else None
+
+    t_step = sum(step_ms) / len(step_ms)
+    if P > 1:
+        t = torch.tensor([t_step], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+    value = N_OPS * E / (t_step * 1e-3) / 1e9
+
+    # ---------------------------------------------------------------- e2e
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        hin = [torch.empty((ncols, F), dtype=torch.float32).pin_memory() for _ in range(4)]
+        for h, d in zip(hin, (X, dY, Z, dO)):
+            h.copy_(d.cpu())
+        hout = [torch.empty((R, F), dtype=torch.float32).pin_memory() for _ in range(4)]
+        dins = (X, dY, Z, dO)
+
+        def e2e_step():
+            for h, d in zip(hin, dins):
+                d.copy_(h, non_blocking=True)
+            step(False)
+            for h, o in zip(hout, outs):
+                h.copy_(o, non_blocking=True)
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        e_ms = []
+        for _ in range(max(3, args.steps // 2)):
+            flush.fill_(1.0)
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            e2e_step()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            e_ms.append(a0.elapsed_time(a1))
+        t_e2e = sum(e_ms) / len(e_ms)
+        if P > 1:
+            t = torch.tensor([t_e2e], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        e2e = {"value": round(N_OPS * E / (t_e2e * 1e-3) / 1e9, 4), "unit": "GE/s",
+               "ms_per_step": round(t_e2e, 4),
+               "h2d_bytes_per_step": int(sum(h.numel() * 4 for h in hin)),
+               "d2h_bytes_per_step": int(sum(h.numel() * 4 for h in hout))}
+
+    # ----------------------------------------------------------- roofline
+    peak, peak_kind = load_peaks()
+    avg = {k: (sum(v) / len(v) if v else None) for k, v in ev.items()}
+    Vloc, Eloc = (R, Ep) if P > 1 else (V, E)
+    per_op = {}
+    bytes_of = {"gspmm_fwd": alg_bytes("gspmm", Vloc, Eloc, F, H), "gspmm_rev": alg_bytes("gspmm", Vloc, Eloc, F, H),
+                "gsddmm": alg_bytes("gsddmm", Vloc, Eloc, F, H),
+                "edge_softmax": alg_bytes("edge_softmax", Vloc, Eloc, F, H),
+                "gspmm_weighted_fwd": alg_bytes("gspmm_weighted_fwd", Vloc, Eloc, F, H),
+                "gspmm_weighted_rev": alg_bytes("gspmm_weighted_rev", Vloc, Eloc, F, H)}
+    for k in op_names:
+        ms = avg[k]
+        gbs = bytes_of[k] / (ms * 1e-3) / 1e9
+        per_op[k] = {"ms": round(ms, 4), "GE_s": round(Eloc / (ms * 1e-3) / 1e9, 3), "alg_GB": round(bytes_of[k] / 1e9, 3),
+                     "GB_s": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
+                     "frac_of_8TBs": round(gbs / 8000.0, 4)}
+    if P > 1:
+        per_op["allgather"] = {"ms": round(avg["allgather"], 4)}
+    dom = "gspmm_fwd"
+    achieved = per_op[dom]["GB_s"]
+    roofline = {"bound": "hbm", "kernel": "spmm_kernel<4,16,1,scaled> (gspmm fwd, BOTH)",
+                "achieved": achieved, "peak": peak, "peak_kind": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "alg_bytes_per_launch": bytes_of[dom],
+                "traffic": load_traffic(args.config)}
+
+    cpu = None
+    if rank == 0 and P == 1 and not args.no_cpu_baseline and not args.profile:
+        r = cpu_oracle_bench(V, src, dst, cfg, target_edges=3_000_000, steps=1)
+        cpu = {"value": round(r["value"], 6), "unit": "GE/s", "cores": 1, "kind": "oracle",
+               "sample": f"the step's 6 ops by the fp64 C oracle (1 thread) on the edges of a random "
+                         f"{r['E_sample'] / E:.1%} of destination rows ({r['E_sample']} edges, same graph); "
+                         f"oracle build {r['t_build']:.1f}s not included"}
+
+    if rank == 0:
+        line = {
+            "metric": "gSpMM GE/s & HBM GB/s (% of 8 TB/s), Reddit-shape F=64, 1/2/4/8 B200",
+            "value": round(value, 4), "unit": "GE/s",
+            "n_gpus": P, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}-shaped GCN gSpMM fwd+bwd (BOTH norm) + GAT chain "
+                                   f"(gSDDMM u.v, edge softmax, weighted gSpMM fwd+rev), F={F}, H={H}x{cfg.Fh}",
+                       "V": V, "E": E, "F": F, "H": H, "Fh": cfg.Fh,
+                       "graph": f"Chung-Lu beta={cfg.beta}, seed={cfg.seed:#x}" if cfg.kind == "chung_lu"
+                       else f"R-MAT scale {cfg.scale}, seed={cfg.seed:#x}",
+                       "parallelism": f"row-partition x{P}" if P > 1 else "single GPU",
+                       "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write); "
+                             f"per-step inputs (col ids {4 * E / 1e9:.2f} GB, alpha {4 * E * H / 1e9:.2f} GB) exceed L2",
+                       "edge_visits_per_step": N_OPS * E},
+            "per_op": per_op,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": (6 * args.steps),
+            "clocks": clk,
+            "timing": {"wall_s_timed_region": round(wall, 3), "graph_gen_s": round(t_gen, 2),
+                       "graph_create_s": round(t_create, 2), "device_graph_bytes": G.device_bytes},
+        }
+        if P > 1:
+            line["note"] = ("N>1: weighted reverse runs on the local-edge partition only (round 1); "
+                            "all-gathers of the four vertex outputs included")
+        print(json.dumps(line), flush=True)
+    if P > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ reference arm
+def main_reference(args):
+    """The oracle (as it stands) timed on the host cores on a bounded sample of
+    the same workload.  Under torchrun only rank 0 works."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = datagen.CONFIGS[args.config]
+    V, src, dst = datagen.make_graph(cfg)
+    target = 1_000_000
+    r = cpu_oracle_bench(V, src, dst, cfg, target_edges=target, steps=args.steps, warmup=args.warmup)
+    sample = (f"per step: the 6 ops by the fp64 C oracle (1 thread) on the edges of a random "
+              f"{r['E_sample'] / len(src):.2%} of destination rows ({r['E_sample']} of {len(src)} edges)")
+    line = {
+        "impl": "reference",
+        "metric": "gSpMM GE/s & HBM GB/s (% of 8 TB/s), Reddit-shape F=64, 1/2/4/8 B200",
+        "value": round(r["value"], 6), "unit": "GE/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(r["t_step"] * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}-shaped step (6 sparse ops) on a bounded row sample",
+                   "V": V, "E": int(len(src)), "E_sample": r["E_sample"]},
+        "cpu_baseline": {"value": round(r["value"], 6), "unit": "GE/s", "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(r["value"], 6), "unit": "GE/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        main_reference(args)
+    else:
+        main_gsp(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,203 @@
+/*
+ * gsp.h -- C ABI of the B200-native GraphPy sparse hot path (arxiv 2402.03548).
+ *
+ * The calls follow the paper's system-API table (Table 1:
+ * "status gSpMMv(g, in, out, eFn, Flag)", "gSpMMveid", "gSDDMMvv"; listings
+ * P:733) and its graph APIs (wrap_graph, get_vcount,
+ * get_ecount).  Mapping: gsp_gspmm = gSpMMv with the normalisation flag
+ * generalised to `norm`, reverse = !Forward; gsp_gspmm_weighted
+ * = gSpMMve (reverse=0) / gSpMMveid = gSpMMve^T through the edge ID
+ * (reverse=1); gsp_gsddmm = gSDDMMvv;
+ * gsp_edge_softmax = the per-destination softmax of GAT.
+ *
+ * Conventions (every call):
+ *  - Every call returns gsp_status; nothing aborts or throws across the ABI.
+ *    On error nothing is written and nothing is launched; a detail string is
+ *    available from gsp_last_error_detail() (thread-local).
+ *  - Ownership follows the paper's "Half DLPack" borrowing (P:697-704,
+ *    P:1014-1017): the CALLER allocates every tensor, including outputs, and
+ *    the library never retains a tensor pointer after the call returns.  The
+ *    graph object is library-owned until gsp_graph_destroy.
+ *  - Compute calls allocate nothing and are asynchronous on `stream`
+ *    (GSP_OK means "enqueued"); kernel faults surface as sticky CUDA errors at
+ *    the caller's next synchronisation.  The graph is immutable after create,
+ *    so concurrent compute calls on different streams are safe.
+ *  - Outputs are fully overwritten (rows with no edges become 0), so callers
+ *    need not zero them (the paper's th.zeros, is unnecessary).
+ *  - Edge (u -> v) means A[v][u] = 1; v = destination = "fwd" row, u = source
+ *    = "fwd" column.  The fwd structure groups edges by
+ *    destination (CSR, implicit consecutive edge IDs), the rev structure groups
+ *    them by source (CSC, explicit edge-ID array) -- P:2001-2005 §Storage
+ *    Format "novel edge ID reordering".  Edge tensors are indexed by edge ID.
+ */
+#ifndef GSP_H
+#define GSP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gsp_graph gsp_graph;          /* opaque; owned by the library */
+typedef struct CUstream_st *gsp_stream;      /* == cudaStream_t; NULL = legacy default stream */
+
+/* Borrowed dense fp32 matrix, row-major: element (r, c) is data[r*ld + c].
+ * ld >= cols (elements).  The buffer spans rows*ld floats (padding columns
+ * [cols, ld) may be read but are never written).  The paper's array_t. */
+typedef struct {
+    void *data;
+    int64_t rows, cols, ld;
+} gsp_tensor;
+
+typedef enum {
+    GSP_OK = 0,
+    GSP_ERR_NULL = 1,          /* a required pointer is NULL */
+    GSP_ERR_ARG = 2,           /* bad enum / flag / count, no device, stream on another device */
+    GSP_ERR_VERTEX_RANGE = 3,  /* a COO id is outside [0, V) */
+    GSP_ERR_SHAPE = 4,         /* rows/cols/ld inconsistent with the graph or each other */
+    GSP_ERR_ALIAS = 5,         /* output overlaps an input (edge_softmax allows out == e exactly) */
+    GSP_ERR_NO_REVERSE = 6,    /* reverse op on a graph built without the rev structure */
+    GSP_ERR_OVERFLOW = 7,      /* V or E >= 2^31 (int32 column ids / edge ids) */
+    GSP_ERR_OOM = 8,           /* host or device allocation failed */
+    GSP_ERR_CUDA = 9           /* a CUDA runtime call failed (detail has the CUDA error) */
+} gsp_status;
+
+/* norm ("normalization by degree", reading L1; d^ = max(d,1)):
+ *   NONE : out[v] = sum_u X[u]
+ *   RIGHT: out[v] = 1/d^_in(v) * sum_u X[u]                      (D_in^-1 A, the paper/SPEC form)
+ *   BOTH : out[v] = d^_in(v)^-1/2 * sum_u d^_out(u)^-1/2 X[u]     (D_in^-1/2 A D_out^-1/2, GCN) */
+enum { GSP_NORM_NONE = 0, GSP_NORM_RIGHT = 1, GSP_NORM_BOTH = 2 };
+
+/* gsp_graph_create flags */
+enum {
+    GSP_BUILD_REVERSE = 1u << 0,          /* build the rev (CSC) structure + rev_eid (needed for reverse=1) */
+    GSP_BUILD_SHARE_SYMMETRIC = 1u << 1   /* if the edge multiset is symmetric, keep ONE topology for
+                                             fwd and rev ("one copy of the topology"); rev_eid
+                                             is still stored */
+};
+
+/* gsp_graph_partition flags */
+enum { GSP_PART_REVERSE = 1u << 0 };     /* partition the rev structure (rows = sources) */
+
+/* ------------------------------------------------------------------ graph */
+
+/* Build the kernel-graph from a host COO list (src[i] -> dst[i], i < E) --
+ * GraphPy-SM's get_csr + GraphPy-GNN's wrap_graph in one call.
+ *  fwd: rows = destinations, slots ordered by (dst, src, input position);
+ *       edge ID of slot j is j (implicit).
+ *  rev: rows = sources, slots ordered by (src, dst, edge ID); rev_eid[k] is
+ *       the edge ID of rev slot k.
+ * Duplicates and self-loops are kept as distinct edges (L7).
+ * device >= 0: upload to that CUDA device and precompute the degree scales
+ *   and degree-binned row schedules (synchronous: returns after the upload).
+ * device == -1: host-only graph (structure + export + partitioning; compute
+ *   calls return GSP_ERR_ARG).  src/dst are only read during the call.
+ * Errors: NULL (g_out, or src/dst with E > 0), ARG (V < 0, E < 0, unknown
+ * flags, device out of range), VERTEX_RANGE, OVERFLOW, OOM, CUDA. */
+gsp_status gsp_graph_create(int64_t V, int64_t E, const int64_t *src, const int64_t *dst,
+                            uint32_t flags, int device, gsp_graph **g_out);
+
+/* NULL is a no-op.  Not thread-safe against in-flight compute calls on g:
+ * synchronise the streams that use g first. */
+gsp_status gsp_graph_destroy(gsp_graph *g);
+
+/* get_vcount / get_ecount.  For a partition graph V is the local
+ * row count R (padded) and E the local edge count.  Any output may be NULL.
+ * device_bytes = bytes this graph holds on the device (topology, edge IDs,
+ * scales, schedules); symmetric = 1 if the topology is shared fwd/rev. */
+gsp_status gsp_graph_info(const gsp_graph *g, int64_t *V, int64_t *E, int64_t *device_bytes,
+                          int *symmetric);
+
+/* Copy the canonical structure into caller-allocated HOST arrays (bit-exact
+ * checks).  fwd_off[V+1], fwd_col[E], rev_off[V+1], rev_col[E], rev_eid[E],
+ * coo_to_eid[E] (coo_to_eid[i] = edge ID of input COO edge i).  Any NULL is
+ * skipped.  rev_* on a graph without rev -> GSP_ERR_NO_REVERSE; coo_to_eid or
+ * rev_* on a partition graph -> GSP_ERR_ARG. */
+gsp_status gsp_graph_export(const gsp_graph *g, int64_t *fwd_off, int32_t *fwd_col, int64_t *rev_off,
+                            int32_t *rev_col, int32_t *rev_eid, int32_t *coo_to_eid);
+
+/* ---------------------------------------------------------------- compute */
+
+/* gSpMMv with fused degree normalisation.
+ *  reverse = 0: out[v,f] = s_dst(v) * sum_{slots j of fwd row v} s_src(col_j) * X[col_j, f]
+ *  reverse = 1: out[u,f] = s_src(u) * sum_{slots k of rev row u} s_dst(rcol_k) * X[rcol_k, f]
+ *  (reverse=1 is the exact adjoint of reverse=0 under the same norm: GCN
+ *  backward, with the column-side degree applied per non-zero -- P:1536-1540.)
+ * Shapes: X [ncols, F], out [nrows, F] with F = X->cols = out->cols >= 0;
+ * ncols = nrows = V for a full graph (partition graphs: see gsp_graph_partition).
+ * Errors: NULL, ARG (bad norm/reverse, host-only graph), SHAPE, ALIAS (out
+ * overlaps X), NO_REVERSE, CUDA (launch failure). */
+gsp_status gsp_gspmm(const gsp_graph *g, const gsp_tensor *X, int norm, gsp_tensor *out,
+                     int reverse, gsp_stream stream);
+
+/* Weighted multi-head gSpMM (gSpMMve P:598-601; gSpMMve^T via the
+ * edge ID P:2017-2021).  H = w->cols, Fh = X->cols / H (X->cols % H == 0);
+ * head h of a vertex row is columns [h*Fh, (h+1)*Fh) (L10).
+ *  reverse = 0: out[v, h*Fh+f] = sum_{j in fwd row v} w[j, h] * X[col_j, h*Fh+f]
+ *  reverse = 1: out[u, h*Fh+f] = sum_{k in rev row u} w[rev_eid_k, h] * X[rcol_k, h*Fh+f]
+ * w is [E, H] indexed by edge ID (no eShuffle, no O(E) temporary).
+ * Errors as gsp_gspmm; SHAPE also when w->rows != E or X->cols % H != 0.
+ * Partition graphs: reverse = 0 only (reverse = 1 -> GSP_ERR_NO_REVERSE). */
+gsp_status gsp_gspmm_weighted(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *w,
+                              gsp_tensor *out, int reverse, gsp_stream stream);
+
+/* gSDDMMvv: for every slot j of fwd row v,
+ *   out[j, h] = sum_{f < Fh} X[v, h*Fh+f] * Y[col_j, h*Fh+f],   H = out->cols, Fh = X->cols / H.
+ * X is the destination (row) side, Y the source (column) side; X == Y allowed
+ * (L8).  X and Y are [ncols, H*Fh] (for a partition graph, local row
+ * r reads X row row_base + r of the padded table); out is [E, H] by edge ID.
+ * Errors: NULL, ARG, SHAPE, ALIAS (out overlaps X or Y), CUDA. */
+gsp_status gsp_gsddmm(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *Y, gsp_tensor *out,
+                      gsp_stream stream);
+
+/* Edge softmax over each destination's incoming edges (fwd row), per head
+ * (L9):
+ *   out[j,h] = exp(e[j,h] - m_v,h) / sum_{j' in row v} exp(e[j',h] - m_v,h),  m = row max.
+ * e, out are [E, H]; out == e exactly (same data and ld) is allowed (in place),
+ * any other overlap is GSP_ERR_ALIAS.  Non-finite inputs propagate (IEEE). */
+gsp_status gsp_edge_softmax(const gsp_graph *g, const gsp_tensor *e, gsp_tensor *out, gsp_stream stream);
+
+/* -------------------------------------------------------------- multi-GPU */
+
+/* Edge-balanced contiguous row bounds:
+ * bounds[0] = 0, bounds[nparts] = V, bounds[p] = min{ v : off[v] >= ceil(p*E/nparts) },
+ * off = fwd_off (reverse = 0) or rev_off (reverse = 1).  bounds has nparts+1
+ * entries (caller-allocated, host).  Empty parts are allowed. */
+gsp_status gsp_partition_bounds(const gsp_graph *g, int nparts, int reverse, int64_t *bounds);
+
+/* Partition `part` of `nparts` of a full graph g (rows [b_part, b_part+1) of
+ * the fwd structure, or of the rev structure with GSP_PART_REVERSE), in the
+ * padded rank-major layout: R = max_p (b_{p+1} - b_p); the partition has R
+ * rows (rows past the local count are empty) and every column id v is
+ * remapped to p(v)*R + (v - b_p(v)), so X tables are [nparts*R, F] and one
+ * all-gather of the [R, F] outputs forms the next layer's input.  Local edge
+ * IDs are global edge IDs minus fwd_off[b_part] (fwd partitions).
+ * Compute on a partition graph:
+ *  gsp_gspmm(reverse = 0) on a fwd partition / reverse = 1 on a
+ *  GSP_PART_REVERSE partition gives rows [b_p, b_p+1) of the full op; on a
+ *  symmetric shared graph a fwd partition also serves reverse = 1.
+ *  gsp_gsddmm / gsp_edge_softmax / gsp_gspmm_weighted(reverse=0): fwd
+ *  partitions only; the destination-side table of gsddmm is the padded table.
+ * device as in gsp_graph_create (-1 = host-only).  flags: GSP_PART_REVERSE.
+ * Errors: NULL, ARG (nparts < 1, part out of range, g is itself a partition),
+ * NO_REVERSE, OOM, CUDA. */
+gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int device, uint32_t flags,
+                               gsp_graph **out);
+
+/* Partition geometry (any output may be NULL): nparts, part, global row range
+ * [row_begin, row_end), padded rows R, ncols = nparts*R, reverse = 1 for a
+ * GSP_PART_REVERSE partition.  For a full graph: nparts = 1, part = 0,
+ * [0, V), R = V, ncols = V, reverse = 0. */
+gsp_status gsp_partition_info(const gsp_graph *g, int *nparts, int *part, int64_t *row_begin,
+                              int64_t *row_end, int64_t *R, int64_t *ncols, int *reverse);
+
+/* ------------------------------------------------------------------ misc */
+const char *gsp_status_string(gsp_status st);
+const char *gsp_last_error_detail(void);      /* thread-local; "" if none */
+int gsp_version(void);                          /* (major << 16) | minor */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSP_H */

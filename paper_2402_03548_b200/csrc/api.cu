@@ -1,0 +1,609 @@
+// C ABI of libgsp (include/gsp.h): host-side validation, the device graph
+// object (upload, degree scales, degree-binned schedules, partitions) and the
+// dispatch of the sm_100a kernels.  No exception or abort crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "graph.h"
+#include "gsp.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_detail;
+
+gsp_status fail(gsp_status st, const std::string &msg) {
+    g_detail = msg;
+    return st;
+}
+gsp_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(GSP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess) ok = true;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <class T>
+gsp_status dev_upload(gsp_graph *g, const T *h, size_t n, const T **out) {
+    *out = nullptr;
+    if (n == 0) return GSP_OK;
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(GSP_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    g->dev_allocs.push_back(p);
+    g->device_bytes += (int64_t)(n * sizeof(T));
+    e = cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy H2D");
+    *out = static_cast<const T *>(p);
+    return GSP_OK;
+}
+
+gsp_status dev_alloc_f32(gsp_graph *g, size_t n, float **out) {
+    *out = nullptr;
+    if (n == 0) return GSP_OK;
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(float));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(GSP_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    g->dev_allocs.push_back(p);
+    g->device_bytes += (int64_t)(n * sizeof(float));
+    *out = static_cast<float *>(p);
+    return GSP_OK;
+}
+
+void free_device(gsp_graph *g) {
+    if (g->device >= 0) {
+        DeviceGuard dg(g->device);
+        for (void *p : g->dev_allocs) cudaFree(p);
+    }
+    g->dev_allocs.clear();
+}
+
+// fp32 degree scales (1/d^, d^^-1/2) of an integer degree vector, on the device.
+gsp_status make_scales(gsp_graph *g, const std::vector<int64_t> &deg, const float **inv, const float **rsq) {
+    *inv = *rsq = nullptr;
+    if (deg.empty()) return GSP_OK;
+    const int64_t *d_deg = nullptr;
+    gsp_status st = dev_upload(g, deg.data(), deg.size(), &d_deg);
+    if (st != GSP_OK) return st;
+    float *pi = nullptr, *pr = nullptr;
+    if ((st = dev_alloc_f32(g, deg.size(), &pi)) != GSP_OK) return st;
+    if ((st = dev_alloc_f32(g, deg.size(), &pr)) != GSP_OK) return st;
+    cudaError_t e = gsp::launch_degree_scales(d_deg, (int64_t)deg.size(), pi, pr, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "degree_scales launch");
+    *inv = pi;
+    *rsq = pr;
+    return GSP_OK;
+}
+
+gsp_status upload_structure(gsp_graph *g, gsp::DevStructure &S, int64_t nrows, int64_t ncols,
+                            const std::vector<int64_t> &off, const std::vector<int32_t> &col,
+                            const std::vector<int32_t> *eid, const int32_t *shared_order,
+                            int64_t shared_n_heavy, const gsp::DevStructure *share_topology) {
+    S.nrows = nrows;
+    S.ncols = ncols;
+    S.nnz = off.empty() ? 0 : off.back();
+    S.present = true;
+    gsp_status st;
+    S.max_deg = 0;
+    for (int64_t r = 0; r < nrows; r++) S.max_deg = std::max<int64_t>(S.max_deg, off[r + 1] - off[r]);
+    if (share_topology) {
+        S.off = share_topology->off;
+        S.col = share_topology->col;
+    } else {
+        if ((st = dev_upload(g, off.data(), off.size(), &S.off)) != GSP_OK) return st;
+        if ((st = dev_upload(g, col.data(), col.size(), &S.col)) != GSP_OK) return st;
+    }
+    if (eid && (st = dev_upload(g, eid->data(), eid->size(), &S.eid)) != GSP_OK) return st;
+    if (shared_order) {
+        S.order = shared_order;
+        S.n_heavy = shared_n_heavy;
+    } else {
+        std::vector<int32_t> order;
+        gsp::degree_order(off.data(), nrows, gsp::kHeavyThreshold, order, S.n_heavy);
+        if ((st = dev_upload(g, order.data(), order.size(), &S.order)) != GSP_OK) return st;
+    }
+    return GSP_OK;
+}
+
+std::vector<int64_t> degrees_of(const std::vector<int64_t> &off) {
+    std::vector<int64_t> d(off.empty() ? 0 : off.size() - 1);
+    for (size_t i = 0; i + 1 < off.size(); i++) d[i] = off[i + 1] - off[i];
+    return d;
+}
+
+// ---------------------------------------------------------------- checks
+bool overlaps(const gsp_tensor *a, const gsp_tensor *b) {
+    if (!a || !b || !a->data || !b->data) return false;
+    if (a->rows == 0 || b->rows == 0) return false;
+    auto lo_a = reinterpret_cast<uintptr_t>(a->data), lo_b = reinterpret_cast<uintptr_t>(b->data);
+    auto hi_a = lo_a + (uintptr_t)(a->rows * a->ld) * 4, hi_b = lo_b + (uintptr_t)(b->rows * b->ld) * 4;
+    return lo_a < hi_b && lo_b < hi_a;
+}
+
+gsp_status check_tensor(const gsp_graph *g, const gsp_tensor *t, const char *name, int64_t rows, int64_t cols) {
+    if (!t) return fail(GSP_ERR_NULL, std::string(name) + " is NULL");
+    if (t->rows < 0 || t->cols < 0 || t->ld < t->cols)
+        return fail(GSP_ERR_SHAPE, std::string(name) + ": need rows >= 0, cols >= 0, ld >= cols");
+    if (rows >= 0 && t->rows != rows)
+        return fail(GSP_ERR_SHAPE, std::string(name) + ".rows = " + std::to_string(t->rows) + ", expected " +
+                                       std::to_string(rows));
+    if (cols >= 0 && t->cols != cols)
+        return fail(GSP_ERR_SHAPE, std::string(name) + ".cols = " + std::to_string(t->cols) + ", expected " +
+                                       std::to_string(cols));
+    if (t->rows > 0 && t->cols > 0) {
+        if (!t->data) return fail(GSP_ERR_NULL, std::string(name) + ".data is NULL");
+        cudaPointerAttributes at;
+        cudaError_t e = cudaPointerGetAttributes(&at, t->data);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(GSP_ERR_ARG, std::string(name) + ": not a CUDA pointer");
+        }
+        if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+            return fail(GSP_ERR_ARG, std::string(name) + ": not device memory");
+        if (at.type == cudaMemoryTypeDevice && at.device != g->device)
+            return fail(GSP_ERR_ARG, std::string(name) + ": on device " + std::to_string(at.device) +
+                                         ", graph on device " + std::to_string(g->device));
+    }
+    return GSP_OK;
+}
+
+gsp_status check_compute_graph(const gsp_graph *g) {
+    if (!g) return fail(GSP_ERR_NULL, "graph is NULL");
+    if (g->device < 0) return fail(GSP_ERR_ARG, "host-only graph (device = -1) cannot run compute calls");
+    return GSP_OK;
+}
+
+gsp_status check_stream(const gsp_graph *g, gsp_stream s) {
+    if (!s) return GSP_OK;
+    int dev = -1;
+    cudaError_t e = cudaStreamGetDevice((cudaStream_t)s, &dev);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(GSP_ERR_ARG, std::string("invalid stream: ") + cudaGetErrorString(e));
+    }
+    if (dev != g->device)
+        return fail(GSP_ERR_ARG, "stream on device " + std::to_string(dev) + ", graph on device " +
+                                     std::to_string(g->device));
+    return GSP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *gsp_status_string(gsp_status st) {
+    switch (st) {
+        case GSP_OK: return "GSP_OK";
+        case GSP_ERR_NULL: return "GSP_ERR_NULL";
+        case GSP_ERR_ARG: return "GSP_ERR_ARG";
+        case GSP_ERR_VERTEX_RANGE: return "GSP_ERR_VERTEX_RANGE";
+        case GSP_ERR_SHAPE: return "GSP_ERR_SHAPE";
+        case GSP_ERR_ALIAS: return "GSP_ERR_ALIAS";
+        case GSP_ERR_NO_REVERSE: return "GSP_ERR_NO_REVERSE";
+        case GSP_ERR_OVERFLOW: return "GSP_ERR_OVERFLOW";
+        case GSP_ERR_OOM: return "GSP_ERR_OOM";
+        case GSP_ERR_CUDA: return "GSP_ERR_CUDA";
+    }
+    return "GSP_ERR_UNKNOWN";
+}
+
+const char *gsp_last_error_detail(void) { return g_detail.c_str(); }
+
+int gsp_version(void) { return (1 << 16) | 0; }
+
+static gsp_status upload_full(gsp_graph *g) {
+    const gsp::HostGraph &h = g->host;
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return fail(GSP_ERR_ARG, "cannot select device " + std::to_string(g->device));
+    gsp_status st;
+    std::vector<int64_t> din = degrees_of(h.fwd_off), dout;
+    if (h.has_rev) dout = degrees_of(h.rev_off);
+    else {
+        dout.assign((size_t)h.V, 0);
+        for (int32_t u : h.fwd_col) dout[u]++;
+    }
+    const float *inv_in, *rsq_in, *inv_out, *rsq_out;
+    if ((st = make_scales(g, din, &inv_in, &rsq_in)) != GSP_OK) return st;
+    if ((st = make_scales(g, dout, &inv_out, &rsq_out)) != GSP_OK) return st;
+    (void)inv_out;
+    if ((st = upload_structure(g, g->fwd, h.V, h.V, h.fwd_off, h.fwd_col, nullptr, nullptr, 0, nullptr)) != GSP_OK)
+        return st;
+    g->fwd.row_scale[GSP_NORM_RIGHT] = inv_in;
+    g->fwd.row_scale[GSP_NORM_BOTH] = rsq_in;
+    g->fwd.col_scale[GSP_NORM_BOTH] = rsq_out;
+    if (h.has_rev) {
+        if (h.symmetric)
+            st = upload_structure(g, g->rev, h.V, h.V, h.rev_off, h.rev_col, &h.rev_eid, g->fwd.order,
+                                  g->fwd.n_heavy, &g->fwd);
+        else
+            st = upload_structure(g, g->rev, h.V, h.V, h.rev_off, h.rev_col, &h.rev_eid, nullptr, 0, nullptr);
+        if (st != GSP_OK) return st;
+        g->rev.row_scale[GSP_NORM_BOTH] = rsq_out;
+        g->rev.col_scale[GSP_NORM_RIGHT] = inv_in;
+        g->rev.col_scale[GSP_NORM_BOTH] = rsq_in;
+    }
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "graph upload");
+    return GSP_OK;
+}
+
+gsp_status gsp_graph_create(int64_t V, int64_t E, const int64_t *src, const int64_t *dst, uint32_t flags,
+                            int device, gsp_graph **g_out) {
+    if (!g_out) return fail(GSP_ERR_NULL, "g_out is NULL");
+    *g_out = nullptr;
+    if (E > 0 && (!src || !dst)) return fail(GSP_ERR_NULL, "src/dst is NULL");
+    if (V < 0 || E < 0) return fail(GSP_ERR_ARG, "V and E must be >= 0");
+    if (flags & ~(uint32_t)(GSP_BUILD_REVERSE | GSP_BUILD_SHARE_SYMMETRIC))
+        return fail(GSP_ERR_ARG, "unknown flags");
+    if (V >= (int64_t(1) << 31) || E >= (int64_t(1) << 31))
+        return fail(GSP_ERR_OVERFLOW, "V and E must be < 2^31 (int32 column and edge ids)");
+    if (device < -1) return fail(GSP_ERR_ARG, "device must be >= -1");
+    if (device >= 0) {
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess || device >= n) {
+            cudaGetLastError();
+            return fail(GSP_ERR_ARG, "device " + std::to_string(device) + " not available");
+        }
+    }
+    gsp_graph *g = new (std::nothrow) gsp_graph();
+    if (!g) return fail(GSP_ERR_OOM, "host allocation failed");
+    std::string detail;
+    gsp_status st = gsp::build_host_graph(V, E, src, dst, (flags & GSP_BUILD_REVERSE) != 0, g->host, detail);
+    if (st != GSP_OK) {
+        delete g;
+        return fail(st, detail);
+    }
+    if (!(flags & GSP_BUILD_SHARE_SYMMETRIC)) g->host.symmetric = false;
+    g->nrows = g->ncols = g->V_global = V;
+    g->E = E;
+    g->row_begin = 0;
+    g->row_end = V;
+    g->R = V;
+    g->symmetric = g->host.symmetric;
+    g->device = device;
+    if (device >= 0) {
+        st = upload_full(g);
+        if (st != GSP_OK) {
+            std::string keep = g_detail;
+            free_device(g);
+            delete g;
+            return fail(st, keep);
+        }
+    }
+    *g_out = g;
+    return GSP_OK;
+}
+
+gsp_status gsp_graph_destroy(gsp_graph *g) {
+    if (!g) return GSP_OK;
+    free_device(g);
+    delete g;
+    return GSP_OK;
+}
+
+gsp_status gsp_graph_info(const gsp_graph *g, int64_t *V, int64_t *E, int64_t *device_bytes, int *symmetric) {
+    if (!g) return fail(GSP_ERR_NULL, "graph is NULL");
+    if (V) *V = g->nrows;
+    if (E) *E = g->E;
+    if (device_bytes) *device_bytes = g->device_bytes;
+    if (symmetric) *symmetric = g->symmetric ? 1 : 0;
+    return GSP_OK;
+}
+
+gsp_status gsp_graph_export(const gsp_graph *g, int64_t *fwd_off, int32_t *fwd_col, int64_t *rev_off,
+                            int32_t *rev_col, int32_t *rev_eid, int32_t *coo_to_eid) {
+    if (!g) return fail(GSP_ERR_NULL, "graph is NULL");
+    const gsp::HostGraph &h = g->host;
+    if (g->is_partition && (rev_off || rev_col || rev_eid || coo_to_eid))
+        return fail(GSP_ERR_ARG, "partition graphs export only their own structure (fwd_off, fwd_col)");
+    if ((rev_off || rev_col || rev_eid) && !h.has_rev) return fail(GSP_ERR_NO_REVERSE, "graph has no rev structure");
+    if (fwd_off) std::memcpy(fwd_off, h.fwd_off.data(), sizeof(int64_t) * h.fwd_off.size());
+    if (fwd_col && !h.fwd_col.empty()) std::memcpy(fwd_col, h.fwd_col.data(), sizeof(int32_t) * h.fwd_col.size());
+    if (rev_off) std::memcpy(rev_off, h.rev_off.data(), sizeof(int64_t) * h.rev_off.size());
+    if (rev_col && !h.rev_col.empty()) std::memcpy(rev_col, h.rev_col.data(), sizeof(int32_t) * h.rev_col.size());
+    if (rev_eid && !h.rev_eid.empty()) std::memcpy(rev_eid, h.rev_eid.data(), sizeof(int32_t) * h.rev_eid.size());
+    if (coo_to_eid && !h.coo_to_eid.empty())
+        std::memcpy(coo_to_eid, h.coo_to_eid.data(), sizeof(int32_t) * h.coo_to_eid.size());
+    return GSP_OK;
+}
+
+// ---------------------------------------------------------------- compute
+gsp_status gsp_gspmm(const gsp_graph *g, const gsp_tensor *X, int norm, gsp_tensor *out, int reverse,
+                     gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    if (norm < GSP_NORM_NONE || norm > GSP_NORM_BOTH) return fail(GSP_ERR_ARG, "norm must be 0, 1 or 2");
+    if (reverse != 0 && reverse != 1) return fail(GSP_ERR_ARG, "reverse must be 0 or 1");
+    const gsp::DevStructure &S = reverse ? g->rev : g->fwd;
+    if (!S.present)
+        return reverse ? fail(GSP_ERR_NO_REVERSE, "graph has no rev structure (GSP_BUILD_REVERSE)")
+                       : fail(GSP_ERR_ARG, "this partition only serves reverse = 1");
+    if (!X || !out) return fail(GSP_ERR_NULL, "X/out is NULL");
+    if ((st = check_tensor(g, X, "X", S.ncols, -1)) != GSP_OK) return st;
+    if ((st = check_tensor(g, out, "out", S.nrows, X->cols)) != GSP_OK) return st;
+    if (overlaps(X, out)) return fail(GSP_ERR_ALIAS, "out overlaps X");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    gsp::SpmmArgs a{};
+    a.off = S.off; a.col = S.col; a.eid = nullptr; a.order = S.order;
+    a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
+    a.out = static_cast<float *>(out->data); a.ldo = out->ld;
+    a.F = X->cols;
+    a.row_scale = S.row_scale[norm]; a.col_scale = S.col_scale[norm];
+    a.H = 1; a.Fh = X->cols > 0 ? X->cols : 1;
+    cudaError_t e = gsp::launch_spmm(a, gsp::kSpmmScaled, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gspmm launch");
+    return GSP_OK;
+}
+
+gsp_status gsp_gspmm_weighted(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *w, gsp_tensor *out,
+                              int reverse, gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    if (reverse != 0 && reverse != 1) return fail(GSP_ERR_ARG, "reverse must be 0 or 1");
+    const gsp::DevStructure &S = reverse ? g->rev : g->fwd;
+    if (!S.present || (reverse && !S.eid))
+        return reverse ? fail(GSP_ERR_NO_REVERSE, "no rev structure with edge ids on this graph")
+                       : fail(GSP_ERR_ARG, "this partition only serves reverse = 1");
+    if (!X || !w || !out) return fail(GSP_ERR_NULL, "X/w/out is NULL");
+    if ((st = check_tensor(g, w, "w", g->E, -1)) != GSP_OK) return st;
+    const int64_t H = w->cols;
+    if (H < 1) return fail(GSP_ERR_SHAPE, "w must have H >= 1 columns");
+    if ((st = check_tensor(g, X, "X", S.ncols, -1)) != GSP_OK) return st;
+    if (X->cols % H != 0) return fail(GSP_ERR_SHAPE, "X.cols must be a multiple of H = w.cols");
+    if ((st = check_tensor(g, out, "out", S.nrows, X->cols)) != GSP_OK) return st;
+    if (overlaps(X, out) || overlaps(w, out)) return fail(GSP_ERR_ALIAS, "out overlaps X or w");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    gsp::SpmmArgs a{};
+    a.off = S.off; a.col = S.col; a.eid = S.eid; a.order = S.order;
+    a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
+    a.out = static_cast<float *>(out->data); a.ldo = out->ld;
+    a.F = X->cols;
+    a.w = static_cast<const float *>(w->data); a.ldw = w->ld;
+    a.H = H; a.Fh = X->cols / H > 0 ? X->cols / H : 1;
+    cudaError_t e = gsp::launch_spmm(a, reverse ? gsp::kSpmmWeightedRev : gsp::kSpmmWeightedFwd, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gspmm_weighted launch");
+    return GSP_OK;
+}
+
+gsp_status gsp_gsddmm(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *Y, gsp_tensor *out,
+                      gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    const gsp::DevStructure &S = g->fwd;
+    if (!S.present) return fail(GSP_ERR_ARG, "gsddmm needs the fwd structure (not a reverse partition)");
+    if (!X || !Y || !out) return fail(GSP_ERR_NULL, "X/Y/out is NULL");
+    if ((st = check_tensor(g, out, "out", g->E, -1)) != GSP_OK) return st;
+    const int64_t H = out->cols;
+    if (H < 1) return fail(GSP_ERR_SHAPE, "out must have H >= 1 columns");
+    if ((st = check_tensor(g, X, "X", S.ncols, -1)) != GSP_OK) return st;
+    if ((st = check_tensor(g, Y, "Y", S.ncols, X->cols)) != GSP_OK) return st;
+    if (X->cols % H != 0) return fail(GSP_ERR_SHAPE, "X.cols must be a multiple of H = out.cols");
+    if (overlaps(X, out) || overlaps(Y, out)) return fail(GSP_ERR_ALIAS, "out overlaps X or Y");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    gsp::SddmmArgs a{};
+    a.off = S.off; a.col = S.col; a.order = S.order;
+    a.nrows = S.nrows; a.n_heavy = S.n_heavy; a.row_base = g->row_base;
+    a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
+    a.Y = static_cast<const float *>(Y->data); a.ldy = Y->ld;
+    a.out = static_cast<float *>(out->data); a.ldo = out->ld;
+    a.H = H; a.Fh = X->cols / H;
+    if (a.Fh == 0) {
+        // F = 0: every dot product is empty -> write zeros
+        cudaError_t e = cudaMemset2DAsync(out->data, (size_t)out->ld * 4, 0, (size_t)H * 4, (size_t)g->E,
+                                          (cudaStream_t)stream);
+        if (e != cudaSuccess) return cuda_fail(e, "gsddmm memset");
+        return GSP_OK;
+    }
+    cudaError_t e = gsp::launch_sddmm(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gsddmm launch");
+    return GSP_OK;
+}
+
+gsp_status gsp_edge_softmax(const gsp_graph *g, const gsp_tensor *e_in, gsp_tensor *out, gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    const gsp::DevStructure &S = g->fwd;
+    if (!S.present) return fail(GSP_ERR_ARG, "edge_softmax needs the fwd structure (not a reverse partition)");
+    if (!e_in || !out) return fail(GSP_ERR_NULL, "e/out is NULL");
+    if ((st = check_tensor(g, e_in, "e", g->E, -1)) != GSP_OK) return st;
+    if ((st = check_tensor(g, out, "out", g->E, e_in->cols)) != GSP_OK) return st;
+    const bool same = e_in->data == out->data && e_in->ld == out->ld;
+    if (!same && overlaps(e_in, out)) return fail(GSP_ERR_ALIAS, "out partially overlaps e");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    gsp::SoftmaxArgs a{};
+    a.off = S.off; a.order = S.order; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.e = static_cast<const float *>(e_in->data); a.lde = e_in->ld;
+    a.out = static_cast<float *>(out->data); a.ldo = out->ld;
+    a.H = e_in->cols;
+    cudaError_t err = gsp::launch_softmax(a, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "edge_softmax launch");
+    return GSP_OK;
+}
+
+// -------------------------------------------------------------- partition
+static void bounds_of(const std::vector<int64_t> &off, int64_t V, int nparts, int64_t *bounds) {
+    const int64_t E = off[V];
+    bounds[0] = 0;
+    for (int p = 1; p < nparts; p++) {
+        const int64_t target = (int64_t)(((__int128)p * E + nparts - 1) / nparts);  // ceil(p*E/P)
+        bounds[p] = std::lower_bound(off.begin(), off.begin() + V + 1, target) - off.begin();
+    }
+    bounds[nparts] = V;
+}
+
+gsp_status gsp_partition_bounds(const gsp_graph *g, int nparts, int reverse, int64_t *bounds) {
+    if (!g || !bounds) return fail(GSP_ERR_NULL, "graph/bounds is NULL");
+    if (g->is_partition) return fail(GSP_ERR_ARG, "graph is already a partition");
+    if (nparts < 1) return fail(GSP_ERR_ARG, "nparts must be >= 1");
+    if (reverse != 0 && reverse != 1) return fail(GSP_ERR_ARG, "reverse must be 0 or 1");
+    if (reverse && !g->host.has_rev) return fail(GSP_ERR_NO_REVERSE, "graph has no rev structure");
+    bounds_of(reverse ? g->host.rev_off : g->host.fwd_off, g->host.V, nparts, bounds);
+    return GSP_OK;
+}
+
+gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int device, uint32_t flags,
+                               gsp_graph **out) {
+    if (!g || !out) return fail(GSP_ERR_NULL, "graph/out is NULL");
+    *out = nullptr;
+    if (g->is_partition) return fail(GSP_ERR_ARG, "graph is already a partition");
+    if (nparts < 1 || part < 0 || part >= nparts) return fail(GSP_ERR_ARG, "need 0 <= part < nparts");
+    if (flags & ~(uint32_t)GSP_PART_REVERSE) return fail(GSP_ERR_ARG, "unknown flags");
+    if (device < -1) return fail(GSP_ERR_ARG, "device must be >= -1");
+    const bool prev = (flags & GSP_PART_REVERSE) != 0;
+    const gsp::HostGraph &h = g->host;
+    if (prev && !h.has_rev) return fail(GSP_ERR_NO_REVERSE, "graph has no rev structure");
+    if (device >= 0) {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || device >= n) {
+            cudaGetLastError();
+            return fail(GSP_ERR_ARG, "device " + std::to_string(device) + " not available");
+        }
+    }
+    const std::vector<int64_t> &off = prev ? h.rev_off : h.fwd_off;
+    const std::vector<int32_t> &col = prev ? h.rev_col : h.fwd_col;
+    const int64_t V = h.V;
+    std::vector<int64_t> b((size_t)nparts + 1);
+    bounds_of(off, V, nparts, b.data());
+    int64_t R = 0;
+    for (int p = 0; p < nparts; p++) R = std::max<int64_t>(R, b[p + 1] - b[p]);
+    if ((__int128)nparts * R >= ((__int128)1 << 31)) return fail(GSP_ERR_OVERFLOW, "padded column space >= 2^31");
+    gsp_graph *pg = new (std::nothrow) gsp_graph();
+    if (!pg) return fail(GSP_ERR_OOM, "host allocation failed");
+    try {
+        const int64_t rb = b[part], re = b[part + 1], nloc = re - rb, base = off[rb];
+        std::vector<int32_t> pmap((size_t)V);
+        for (int p = 0; p < nparts; p++)
+            for (int64_t v = b[p]; v < b[p + 1]; v++) pmap[v] = p;
+        auto padded = [&](int64_t v) { return (int64_t)pmap[v] * R + (v - b[pmap[v]]); };
+        gsp::HostGraph &lh = pg->host;
+        lh.V = R;
+        lh.E = off[re] - base;
+        lh.fwd_off.resize((size_t)R + 1);
+        for (int64_t r = 0; r <= R; r++) lh.fwd_off[r] = off[rb + std::min(r, nloc)] - base;
+        lh.fwd_col.resize((size_t)lh.E);
+        for (int64_t j = 0; j < lh.E; j++) lh.fwd_col[j] = (int32_t)padded(col[base + j]);
+        pg->is_partition = true;
+        pg->nparts = nparts;
+        pg->part = part;
+        pg->part_reverse = prev ? 1 : 0;
+        pg->row_begin = rb;
+        pg->row_end = re;
+        pg->R = R;
+        pg->row_base = (int64_t)part * R;
+        pg->nrows = R;
+        pg->ncols = (int64_t)nparts * R;
+        pg->V_global = V;
+        pg->E = lh.E;
+        pg->symmetric = h.symmetric;
+        pg->device = device;
+        if (device >= 0) {
+            DeviceGuard dg(device);
+            gsp_status st;
+            // global degrees; d_out from rev_off or by counting fwd columns
+            std::vector<int64_t> din = degrees_of(h.fwd_off), dout;
+            if (h.has_rev) dout = degrees_of(h.rev_off);
+            else {
+                dout.assign((size_t)V, 0);
+                for (int32_t u : h.fwd_col) dout[u]++;
+            }
+            std::vector<int64_t> loc_in((size_t)R, 1), loc_out((size_t)R, 1);
+            std::vector<int64_t> pad_in((size_t)nparts * R, 1), pad_out((size_t)nparts * R, 1);
+            for (int64_t r = 0; r < nloc; r++) { loc_in[r] = din[rb + r]; loc_out[r] = dout[rb + r]; }
+            for (int64_t v = 0; v < V; v++) { pad_in[padded(v)] = din[v]; pad_out[padded(v)] = dout[v]; }
+            const float *li_inv, *li_rsq, *lo_inv, *lo_rsq, *pi_inv, *pi_rsq, *po_inv, *po_rsq;
+            if ((st = make_scales(pg, loc_in, &li_inv, &li_rsq)) != GSP_OK ||
+                (st = make_scales(pg, loc_out, &lo_inv, &lo_rsq)) != GSP_OK ||
+                (st = make_scales(pg, pad_in, &pi_inv, &pi_rsq)) != GSP_OK ||
+                (st = make_scales(pg, pad_out, &po_inv, &po_rsq)) != GSP_OK) {
+                std::string keep = g_detail;
+                free_device(pg);
+                delete pg;
+                return fail(st, keep);
+            }
+            (void)lo_inv; (void)po_inv;
+            gsp::DevStructure *fw = prev ? nullptr : &pg->fwd;
+            if (fw) {
+                st = upload_structure(pg, *fw, R, (int64_t)nparts * R, lh.fwd_off, lh.fwd_col, nullptr, nullptr, 0,
+                                      nullptr);
+                if (st == GSP_OK) {
+                    fw->row_scale[GSP_NORM_RIGHT] = li_inv;
+                    fw->row_scale[GSP_NORM_BOTH] = li_rsq;
+                    fw->col_scale[GSP_NORM_BOTH] = po_rsq;
+                }
+            }
+            // rev view: a GSP_PART_REVERSE partition, or the shared topology of a symmetric graph
+            if (st == GSP_OK && (prev || h.symmetric)) {
+                if (prev)
+                    st = upload_structure(pg, pg->rev, R, (int64_t)nparts * R, lh.fwd_off, lh.fwd_col, nullptr,
+                                          nullptr, 0, nullptr);
+                else
+                    st = upload_structure(pg, pg->rev, R, (int64_t)nparts * R, lh.fwd_off, lh.fwd_col, nullptr,
+                                          pg->fwd.order, pg->fwd.n_heavy, &pg->fwd);
+                if (st == GSP_OK) {
+                    pg->rev.eid = nullptr;  // weighted reverse on partitions: not provided
+                    pg->rev.row_scale[GSP_NORM_BOTH] = lo_rsq;
+                    pg->rev.col_scale[GSP_NORM_RIGHT] = pi_inv;
+                    pg->rev.col_scale[GSP_NORM_BOTH] = pi_rsq;
+                }
+            }
+            if (st == GSP_OK) {
+                cudaError_t e = cudaDeviceSynchronize();
+                if (e != cudaSuccess) st = cuda_fail(e, "partition upload");
+            }
+            if (st != GSP_OK) {
+                std::string keep = g_detail;
+                free_device(pg);
+                delete pg;
+                return fail(st, keep);
+            }
+        }
+    } catch (const std::bad_alloc &) {
+        free_device(pg);
+        delete pg;
+        return fail(GSP_ERR_OOM, "host allocation failed in partition");
+    }
+    *out = pg;
+    return GSP_OK;
+}
+
+gsp_status gsp_partition_info(const gsp_graph *g, int *nparts, int *part, int64_t *row_begin, int64_t *row_end,
+                              int64_t *R, int64_t *ncols, int *reverse) {
+    if (!g) return fail(GSP_ERR_NULL, "graph is NULL");
+    if (nparts) *nparts = g->nparts;
+    if (part) *part = g->part;
+    if (row_begin) *row_begin = g->row_begin;
+    if (row_end) *row_end = g->row_end;
+    if (R) *R = g->R;
+    if (ncols) *ncols = g->ncols;
+    if (reverse) *reverse = g->part_reverse;
+    return GSP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// Internal types of libgsp (not part of the ABI; see include/gsp.h).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "gsp.h"
+
+namespace gsp {
+
+// ---------------------------------------------------------------- host side
+// Canonical host structure produced by the builder.
+struct HostGraph {
+    int64_t V = 0, E = 0;
+    std::vector<int64_t> fwd_off;      // [V+1]
+    std::vector<int32_t> fwd_col;      // [E]   source id of fwd slot j (edge ID j)
+    std::vector<int64_t> rev_off;      // [V+1] (empty when no rev)
+    std::vector<int32_t> rev_col;      // [E]   destination id of rev slot k
+    std::vector<int32_t> rev_eid;      // [E]   edge ID of rev slot k
+    std::vector<int32_t> coo_to_eid;   // [E]
+    bool has_rev = false;
+    bool symmetric = false;            // rev topology == fwd topology
+};
+
+// Builds the structure of gsp_graph_create (threads: deterministic result for
+// any thread count).  Returns GSP_OK / GSP_ERR_VERTEX_RANGE / GSP_ERR_OOM.
+gsp_status build_host_graph(int64_t V, int64_t E, const int64_t *src, const int64_t *dst,
+                            bool want_rev, HostGraph &hg, std::string &detail);
+
+// Rows ordered by descending degree (ties: ascending row id); heavy rows
+// (degree > heavy_threshold) come first.  Returned counts: n_heavy.
+void degree_order(const int64_t *off, int64_t nrows, int64_t heavy_threshold,
+                  std::vector<int32_t> &order, int64_t &n_heavy);
+
+// --------------------------------------------------------------- device side
+// One CSR-like structure on the device: `nrows` rows over a column space of
+// `ncols` vertices.  eid == nullptr means implicit edge IDs (slot + eid_base).
+struct DevStructure {
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    const int64_t *off = nullptr;
+    const int32_t *col = nullptr;
+    const int32_t *eid = nullptr;
+    // degree scales per norm: index 0 NONE (null), 1 RIGHT, 2 BOTH; null => 1.0
+    const float *row_scale[3] = {nullptr, nullptr, nullptr};
+    const float *col_scale[3] = {nullptr, nullptr, nullptr};
+    // degree-binned schedule: rows by descending degree; the first n_heavy
+    // rows get a whole CTA each, the rest one warp each.
+    const int32_t *order = nullptr;
+    int64_t n_heavy = 0;
+    int64_t max_deg = 0;
+    bool present = false;
+};
+
+constexpr int64_t kHeavyThreshold = 1024;   // edges; see DESIGN.md "Degree bins"
+
+}  // namespace gsp
+
+struct gsp_graph {
+    int device = -1;
+    int64_t nrows = 0, ncols = 0, E = 0;       // nrows = V (full) or R (partition)
+    int64_t V_global = 0;
+    bool symmetric = false;
+    // partition geometry
+    bool is_partition = false;
+    int nparts = 1, part = 0, part_reverse = 0;
+    int64_t row_begin = 0, row_end = 0, R = 0, row_base = 0;
+    // host mirror (full graphs: HostGraph; partitions: local fwd only)
+    gsp::HostGraph host;
+    // device
+    gsp::DevStructure fwd, rev;
+    std::vector<void *> dev_allocs;
+    int64_t device_bytes = 0;
+};

@@ -1,0 +1,64 @@
+// Host-side launchers of the sm_100a kernels (kernels.cu).  Internal.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace gsp {
+
+// One pass of a gather-reduce over a structure (gSpMMv / gSpMMve / gSpMMve^T).
+struct SpmmArgs {
+    const int64_t *off;
+    const int32_t *col;
+    const int32_t *eid;      // MODE weighted-rev: explicit edge IDs; else unused
+    const int32_t *order;    // degree-ordered rows
+    int64_t nrows, n_heavy;
+    const float *X;
+    int64_t ldx;
+    float *out;
+    int64_t ldo;
+    int64_t F;
+    const float *row_scale;  // may be null (1.0)
+    const float *col_scale;  // may be null (1.0)
+    const float *w;          // weighted modes
+    int64_t ldw;
+    int64_t H, Fh;
+};
+
+enum SpmmMode { kSpmmScaled = 0, kSpmmWeightedFwd = 1, kSpmmWeightedRev = 2 };
+
+cudaError_t launch_spmm(const SpmmArgs &a, int mode, cudaStream_t s);
+
+struct SddmmArgs {
+    const int64_t *off;
+    const int32_t *col;
+    const int32_t *order;
+    int64_t nrows, n_heavy;
+    int64_t row_base;        // X row of local row r is row_base + r
+    const float *X;
+    int64_t ldx;
+    const float *Y;
+    int64_t ldy;
+    float *out;
+    int64_t ldo;
+    int64_t H, Fh;
+};
+cudaError_t launch_sddmm(const SddmmArgs &a, cudaStream_t s);
+
+struct SoftmaxArgs {
+    const int64_t *off;
+    const int32_t *order;
+    int64_t nrows, n_heavy;
+    const float *e;
+    int64_t lde;
+    float *out;
+    int64_t ldo;
+    int64_t H;
+};
+cudaError_t launch_softmax(const SoftmaxArgs &a, cudaStream_t s);
+
+// fp32 degree scales from (clamped) integer degrees: inv = 1/d^, rsq = d^^-1/2
+// computed in fp64 then rounded once.
+cudaError_t launch_degree_scales(const int64_t *deg, int64_t n, float *inv, float *rsq, cudaStream_t s);
+
+}  // namespace gsp

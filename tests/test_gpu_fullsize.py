@@ -1,0 +1,113 @@
+"""Parity at BASELINE.json's full sizes (Reddit- and ogbn-products-shaped), in the
+launch configuration bench.py times: the whole structure bit-exact against the
+oracle's own build, float outputs on sampled rows the oracle computes one by
+one (the heaviest rows -- CTA-split path --, random rows, the lightest rows),
+plus properties that hold at any size (softmax rows sum to 1)."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def sample_rows(off, seed, n_heavy=16, n_rand=48, n_light=16):
+    deg = np.diff(off)
+    order = np.argsort(-deg, kind="stable")
+    rng = np.random.default_rng(seed)
+    rows = np.concatenate([order[:n_heavy], rng.choice(len(deg), n_rand, replace=False), order[-n_light:]])
+    return np.unique(rows).astype(np.int64)
+
+
+def within(gpu, ref, T, scale=1e-5):
+    err = np.abs(np.asarray(gpu, np.float64) - ref)
+    r = float(np.max(err / (scale * (np.asarray(T) + 1.0)))) if err.size else 0.0
+    assert r <= 1.0, f"max err/bound {r:.3g}"
+    return r
+
+
+@pytest.fixture(scope="module")
+def reddit():
+    import paper_2402_03548_b200 as gsp
+    cfg = datagen.CONFIGS["reddit"]
+    V, src, dst = datagen.make_graph(cfg)
+    G = gsp.Graph(V, src, dst, device=0)
+    og = oracle.Graph(V, src, dst)
+    return cfg, G, og
+
+
+def test_reddit_structure_bitexact(reddit):
+    cfg, G, og = reddit
+    assert G.symmetric and G.E == cfg.E
+    ex = G.export()
+    for k in ("fwd_off", "fwd_col", "rev_off", "rev_col", "rev_eid", "coo_to_eid"):
+        assert np.array_equal(ex[k], getattr(og, k)), k
+
+
+@pytest.mark.parametrize("F,ld", [(64, 64), (602, 604)])
+def test_reddit_gspmm_sampled(reddit, F, ld):
+    cfg, G, og = reddit
+    rows = sample_rows(og.fwd_off, F)
+    buf = np.zeros((og.V, ld), np.float32)
+    Xh = datagen.uniform(0x2EDD + F, og.V, F, ld=ld)
+    buf[:] = Xh
+    X = dev(buf)[:, :F]
+    for rev in (0, 1):
+        out = G.gspmm(X, 2, reverse=rev).cpu().numpy()
+        ref, T = og.gspmm(Xh, 2, bool(rev), rows=rows, F=F)
+        within(out[rows], ref, T)
+    # non-negative inputs: the fp32 error-growth case
+    Xp = datagen.uniform(5, og.V, F, ld=ld, lo=0.0, hi=1.0)
+    out = G.gspmm(dev(Xp)[:, :F], 2).cpu().numpy()
+    ref, T = og.gspmm(Xp, 2, False, rows=rows, F=F)
+    within(out[rows], ref, T)
+
+
+def test_reddit_gat_chain_sampled(reddit):
+    cfg, G, og = reddit
+    H, F = cfg.H, cfg.H * cfg.Fh
+    rows = sample_rows(og.fwd_off, 77)
+    eids = og.row_edges(rows)
+    Zh = datagen.uniform(11, og.V, F)
+    Z = dev(Zh)
+    s = G.gsddmm(Z, Z, H=H)
+    ref, T = og.gsddmm(Zh, Zh, H, rows=rows)
+    within(s[torch.from_numpy(eids).cuda()].cpu().numpy(), ref, T)
+    del s
+    lh = datagen.uniform(12, og.E, H, lo=-8, hi=8)
+    a = G.edge_softmax(dev(lh))
+    within(a[torch.from_numpy(eids).cuda()].cpu().numpy(), og.edge_softmax(lh, rows=rows), 1.0)
+    # every non-empty row sums to 1 (any size)
+    rowsum = torch.zeros((og.V, H), dtype=torch.float64, device="cuda")
+    rid = torch.repeat_interleave(torch.arange(og.V, device="cuda"), dev(np.diff(og.fwd_off)))
+    rowsum.index_add_(0, rid, a.double())
+    assert torch.allclose(rowsum, torch.ones_like(rowsum), atol=1e-4)
+    del a, rowsum, rid
+    wh = datagen.uniform(13, og.E, H, lo=0, hi=1)
+    w = dev(wh)
+    for rev in (0, 1):
+        out = G.gspmm_weighted(Z, w, reverse=rev).cpu().numpy()
+        ref, T = og.gspmm_weighted(Zh, wh, bool(rev), rows=rows)
+        within(out[rows], ref, T)
+
+
+def test_products_gspmm_sampled():
+    import paper_2402_03548_b200 as gsp
+    cfg = datagen.CONFIGS["products"]
+    V, src, dst = datagen.make_graph(cfg)
+    G = gsp.Graph(V, src, dst, device=0)
+    og = oracle.Graph(V, src, dst)
+    ex = G.export(rev=False, coo=False)
+    assert np.array_equal(ex["fwd_off"], og.fwd_off) and np.array_equal(ex["fwd_col"], og.fwd_col)
+    rows = sample_rows(og.fwd_off, 3)
+    Xh = datagen.uniform(0x960D, V, cfg.F, ld=cfg.ld)
+    out = G.gspmm(dev(Xh), 2).cpu().numpy()
+    ref, T = og.gspmm(Xh, 2, False, rows=rows)
+    within(out[rows], ref, T)

@@ -1,0 +1,360 @@
+"""GPU parity: the sm_100a kernels behind the C ABI vs the CPU oracle, element by
+element, on the same seeded inputs.  Acceptance (BASELINE.json north_star):
+structure bit-exact; |gpu - oracle| <= 1e-5 * (sum|terms| + 1) per fp32 element
+(edge softmax: T := 1, i.e. 2e-5 absolute -- DESIGN.md "Tolerances")."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+NORMS = (0, 1, 2)
+
+
+@pytest.fixture(scope="module")
+def gsp():
+    import paper_2402_03548_b200 as m
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def padded(a, ld):
+    """fp32 [rows, ld] device tensor holding `a` in its first cols (padding = NaN:
+    the kernels may read padding but must never use it)."""
+    rows, cols = a.shape
+    buf = np.full((rows, ld), np.nan, np.float32)
+    buf[:, :cols] = a
+    t = dev(buf)
+    return t[:, :cols]
+
+
+def assert_within(gpu, ref, T, what="", scale=1e-5):
+    gpu = np.asarray(gpu, np.float64)
+    err = np.abs(gpu - ref)
+    bound = scale * (np.asarray(T) + 1.0)
+    ratio = float(np.max(err / bound)) if err.size else 0.0
+    assert np.all(np.isfinite(gpu)), what
+    assert ratio <= 1.0, f"{what}: max err/bound = {ratio:.3g}"
+    return ratio
+
+
+def graph_pair(gsp, V, src, dst, **kw):
+    return gsp.Graph(V, src, dst, device=0, **kw), oracle.Graph(V, src, dst)
+
+
+# ------------------------------------------------------------------ golden
+def test_golden_t4_d4(gsp, golden):
+    for gf, cf in [("t4.json", "t4_chain.json"), ("d4.json", "d4.json")]:
+        g, c = golden(gf), golden(cf)
+        G, og = graph_pair(gsp, g["V"], g["src"], g["dst"])
+        X = dev(np.array(c["X"], np.float32)[:, None])
+        Y = dev(np.array(c["Y"], np.float32)[:, None])
+        for norm in NORMS:
+            for rev in (0, 1):
+                ref, T = og.gspmm(X.cpu().numpy(), norm, rev)
+                assert_within(G.gspmm(X, norm, reverse=rev).cpu().numpy(), ref, T, f"{gf} n{norm} r{rev}")
+        s = G.gsddmm(X, Y, H=1)
+        assert np.array_equal(s.cpu().numpy()[:, 0], np.array(c["gsddmm_XY"], np.float32))
+        a = G.edge_softmax(s / 100.0)
+        assert np.allclose(a.cpu().numpy()[:, 0], c["edge_softmax_gsddmm_over_100"], atol=2e-5)
+        f = G.gspmm_weighted(X, a).cpu().numpy()[:, 0]
+        r = G.gspmm_weighted(X, a, reverse=True).cpu().numpy()[:, 0]
+        assert np.allclose(f, c["weighted_fwd_alpha_X"], atol=1e-4)
+        assert np.allclose(r, c["weighted_rev_alpha_X"], atol=1e-4)
+
+
+def test_export_matches_oracle_on_device_graph(gsp):
+    V, src, dst = datagen.make_graph("arxiv")
+    G, og = graph_pair(gsp, V, src, dst)
+    ex = G.export()
+    for k in ("fwd_off", "fwd_col", "rev_off", "rev_col", "rev_eid", "coo_to_eid"):
+        assert np.array_equal(ex[k], getattr(og, k)), k
+    assert G.device_bytes > 0
+
+
+# ------------------------------------------------------------- gspmm family
+GSPMM_SHAPES = [(1, 1), (3, 3), (4, 4), (5, 8), (16, 16), (64, 64), (100, 100), (128, 132), (602, 604)]
+
+
+@pytest.mark.parametrize("F,ld", GSPMM_SHAPES)
+def test_gspmm_random_graphs(gsp, F, ld):
+    for seed in range(3):
+        rng = np.random.default_rng(seed * 7 + F)
+        V = int(rng.integers(1, 3000))
+        E = int(rng.integers(0, 40000))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed != 1
+                    else datagen.skewed_multigraph(V, E, seed))
+        G, og = graph_pair(gsp, V, src, dst)
+        Xh = datagen.uniform(seed + 11, V, F)
+        X = padded(Xh, ld)
+        for norm in NORMS:
+            for rev in (0, 1):
+                ref, T = og.gspmm(Xh, norm, rev)
+                out = padded(np.zeros((V, F), np.float32), ld)
+                G.gspmm(X, norm, out=out, reverse=rev)
+                assert_within(out.cpu().numpy(), ref, T, f"V{V} E{E} F{F} n{norm} r{rev}")
+                if ld > F:   # padding columns of out are never written
+                    full = out.as_strided((V, ld), (ld, 1)).cpu().numpy()
+                    assert np.all(np.isnan(full[:, F:]))
+
+
+def test_gspmm_heavy_and_mega_rows(gsp):
+    """Rows far above the 1024-edge CTA threshold (CTA-split path), rows in every
+    degree bin, isolated vertices; non-negative inputs (the error-growth case of
+    SURVEY Appendix B)."""
+    V, E = 4000, 600_000
+    src, dst = datagen.skewed_multigraph(V, E, 3, alpha=1.6)
+    G, og = graph_pair(gsp, V, src, dst)
+    assert np.diff(og.fwd_off).max() > 50_000
+    for F in (16, 64, 128):
+        Xh = datagen.uniform(5, V, F, lo=0.0, hi=1.0)
+        X = dev(Xh)
+        for norm in NORMS:
+            for rev in (0, 1):
+                ref, T = og.gspmm(Xh, norm, rev)
+                assert_within(G.gspmm(X, norm, reverse=rev).cpu().numpy(), ref, T, f"F{F} n{norm} r{rev}")
+
+
+@pytest.mark.parametrize("H,Fh,ld", [(1, 1, 1), (1, 3, 3), (2, 3, 6), (2, 4, 8), (8, 8, 64), (8, 8, 68),
+                                     (4, 16, 64), (3, 5, 15), (1, 64, 64), (2, 64, 128)])
+def test_weighted_random(gsp, H, Fh, ld):
+    for seed in range(2):
+        rng = np.random.default_rng(seed + 31 * H + Fh)
+        V = int(rng.integers(1, 2500))
+        E = int(rng.integers(0, 30000))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed == 0
+                    else datagen.skewed_multigraph(V, E, seed, alpha=1.4))
+        G, og = graph_pair(gsp, V, src, dst)
+        F = H * Fh
+        Xh = datagen.uniform(seed + 3, V, F)
+        wh = datagen.uniform(seed + 4, E, H, lo=0.0, hi=1.0) if E else np.zeros((0, H), np.float32)
+        X, w = padded(Xh, ld), dev(wh)
+        for rev in (0, 1):
+            ref, T = og.gspmm_weighted(Xh, wh, rev)
+            assert_within(G.gspmm_weighted(X, w, reverse=rev).cpu().numpy(), ref, T, f"H{H} Fh{Fh} r{rev}")
+
+
+def test_weighted_heavy_rows(gsp):
+    V, E = 3000, 400_000
+    src, dst = datagen.skewed_multigraph(V, E, 9, alpha=1.6)
+    G, og = graph_pair(gsp, V, src, dst)
+    Xh = datagen.uniform(1, V, 64)
+    wh = datagen.uniform(2, E, 8, lo=0.0, hi=1.0)
+    for rev in (0, 1):
+        ref, T = og.gspmm_weighted(Xh, wh, rev)
+        assert_within(G.gspmm_weighted(dev(Xh), dev(wh), reverse=rev).cpu().numpy(), ref, T, f"r{rev}")
+
+
+# ------------------------------------------------------------------ gsddmm
+@pytest.mark.parametrize("H,Fh,ld", [(1, 1, 1), (1, 3, 3), (2, 3, 6), (2, 4, 8), (8, 8, 64), (8, 8, 72),
+                                     (1, 32, 32), (4, 16, 64), (1, 128, 128), (2, 256, 512), (3, 5, 16)])
+def test_gsddmm_random(gsp, H, Fh, ld):
+    for seed in range(2):
+        rng = np.random.default_rng(seed + 7 * H + Fh)
+        V = int(rng.integers(1, 2500))
+        E = int(rng.integers(0, 30000))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed == 0
+                    else datagen.skewed_multigraph(V, E, seed, alpha=1.5))
+        G, og = graph_pair(gsp, V, src, dst)
+        F = H * Fh
+        Xh = datagen.uniform(seed + 1, V, F)
+        Yh = datagen.uniform(seed + 2, V, F)
+        ref, T = og.gsddmm(Xh, Yh, H)
+        out = G.gsddmm(padded(Xh, ld), padded(Yh, ld), H=H)
+        assert_within(out.cpu().numpy(), ref, T, f"H{H} Fh{Fh}")
+
+
+# ------------------------------------------------------------ edge softmax
+@pytest.mark.parametrize("H,ld", [(1, 1), (2, 2), (3, 3), (4, 4), (8, 8), (8, 12), (16, 16), (32, 32), (5, 7)])
+def test_softmax_random(gsp, H, ld):
+    for seed in range(2):
+        rng = np.random.default_rng(seed + H)
+        V = int(rng.integers(1, 2500))
+        E = int(rng.integers(0, 40000))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed == 0
+                    else datagen.skewed_multigraph(V, E, seed, alpha=1.7))
+        G, og = graph_pair(gsp, V, src, dst)
+        eh = datagen.uniform(seed, E, H, lo=-10.0, hi=10.0) if E else np.zeros((0, H), np.float32)
+        ref = og.edge_softmax(eh)
+        out = G.edge_softmax(padded(eh, ld))
+        assert_within(out.cpu().numpy(), ref, 1.0, f"H{H} ld{ld}")
+
+
+def test_softmax_in_place_and_rows_sum_to_one(gsp):
+    V, E = 3000, 500_000
+    src, dst = datagen.skewed_multigraph(V, E, 4, alpha=1.6)
+    G, og = graph_pair(gsp, V, src, dst)
+    eh = datagen.uniform(3, E, 8, lo=-10.0, hi=10.0)
+    ref = og.edge_softmax(eh)
+    e = dev(eh)
+    G.edge_softmax(e, out=e)                                  # in place (out == e allowed)
+    a = e.cpu().numpy()
+    assert_within(a, ref, 1.0, "in-place")
+    rows = np.repeat(np.arange(V), np.diff(og.fwd_off))
+    sums = np.zeros((V, 8))
+    np.add.at(sums, rows, a.astype(np.float64))
+    nonempty = np.diff(og.fwd_off) > 0
+    assert np.allclose(sums[nonempty], 1.0, atol=1e-4)
+
+
+# ---------------------------------------------------------------- configs
+def test_cora_gcn_fwd_bwd(gsp):
+    cfg = datagen.CONFIGS["cora"]
+    V, src, dst = datagen.make_graph(cfg)
+    G, og = graph_pair(gsp, V, src, dst)
+    Xh = datagen.uniform(1, V, cfg.F)
+    dYh = datagen.uniform(2, V, cfg.F)
+    ref, T = og.gspmm(Xh, 2, False)
+    assert_within(G.gspmm(dev(Xh), 2).cpu().numpy(), ref, T, "cora fwd")
+    ref, T = og.gspmm(dYh, 2, True)
+    assert_within(G.gspmm(dev(dYh), 2, reverse=True).cpu().numpy(), ref, T, "cora bwd")
+
+
+def test_pubmed_gat_chain(gsp):
+    cfg = datagen.CONFIGS["pubmed"]
+    V, src, dst = datagen.make_graph(cfg)
+    G, og = graph_pair(gsp, V, src, dst)
+    H, F = cfg.H, cfg.H * cfg.Fh
+    Zh = datagen.uniform(1, V, F)
+    ref, T = og.gsddmm(Zh, Zh, H)
+    Z = dev(Zh)
+    s = G.gsddmm(Z, Z, H=H)
+    assert_within(s.cpu().numpy(), ref, T, "pubmed gsddmm")
+    lh = datagen.uniform(2, og.E, H, lo=-8, hi=8)
+    assert_within(G.edge_softmax(dev(lh)).cpu().numpy(), og.edge_softmax(lh), 1.0, "pubmed softmax")
+    wh = datagen.uniform(3, og.E, H, lo=0, hi=1)
+    for rev in (0, 1):
+        ref, T = og.gspmm_weighted(Zh, wh, rev)
+        assert_within(G.gspmm_weighted(Z, dev(wh), reverse=rev).cpu().numpy(), ref, T, f"pubmed w r{rev}")
+    # the chain itself (scores -> softmax -> aggregate) vs the oracle's chain, fp32 hand-off;
+    # tolerance derived in DESIGN.md "Tolerances" (score error x softmax sensitivity)
+    a = G.edge_softmax(s)
+    out = G.gspmm_weighted(Z, a).cpu().numpy()
+    a_ref = og.edge_softmax(ref.astype(np.float32))
+    o_ref, oT = og.gspmm_weighted(Zh, a_ref.astype(np.float32))
+    assert_within(out, o_ref, oT, "pubmed chain", scale=1e-3)
+
+
+def test_arxiv_directed_fwd_bwd(gsp):
+    cfg = datagen.CONFIGS["arxiv"]
+    V, src, dst = datagen.make_graph(cfg)
+    G, og = graph_pair(gsp, V, src, dst)
+    assert not G.symmetric
+    Xh = datagen.uniform(1, V, cfg.F)
+    for norm in NORMS:
+        for rev in (0, 1):
+            ref, T = og.gspmm(Xh, norm, rev)
+            assert_within(G.gspmm(dev(Xh), norm, reverse=rev).cpu().numpy(), ref, T, f"arxiv n{norm} r{rev}")
+
+
+# ------------------------------------------------------------- partitions
+@pytest.mark.parametrize("name", ["cora", "arxiv"])
+def test_partitions_simulated_on_one_gpu(gsp, name):
+    """P partitions run one after another on one GPU; the 'all-gather' is a copy
+    into the padded [P*R, F] table.  Concatenated outputs == full oracle."""
+    cfg = datagen.CONFIGS[name]
+    V, src, dst = datagen.make_graph(cfg)
+    G, og = graph_pair(gsp, V, src, dst)
+    F = 16
+    Xh = datagen.uniform(7, V, F)
+    for P in (2, 3, 4):
+        for rev in ((0, 1) if not G.symmetric else (0,)):
+            parts = [G.partition(P, p, device=0, reverse=bool(rev)) for p in range(P)]
+            R = parts[0].R
+            b = G.partition_bounds(P, bool(rev))
+            Xpad = torch.zeros((P * R, F), device="cuda")
+            for p in range(P):
+                Xpad[p * R:p * R + b[p + 1] - b[p]] = dev(Xh[b[p]:b[p + 1]])
+            for norm in NORMS:
+                full, T = og.gspmm(Xh, norm, bool(rev))
+                gathered = torch.zeros((P * R, F), device="cuda")
+                for p, pg in enumerate(parts):
+                    pg.gspmm(Xpad, norm, out=gathered[p * R:(p + 1) * R], reverse=rev)
+                    if G.symmetric:   # shared topology also serves the reverse op
+                        ref_r, Tr = og.gspmm(Xh, norm, True)
+                        o = pg.gspmm(Xpad, norm, reverse=1).cpu().numpy()
+                        n = b[p + 1] - b[p]
+                        assert_within(o[:n], ref_r[b[p]:b[p + 1]], Tr[b[p]:b[p + 1]], "sym rev part")
+                        assert np.all(o[n:] == 0)
+                g = gathered.cpu().numpy()
+                got = np.concatenate([g[p * R:p * R + b[p + 1] - b[p]] for p in range(P)])
+                assert_within(got, full, T, f"{name} P{P} n{norm} r{rev}")
+
+
+def test_partition_gat_chain_blocks(gsp):
+    cfg = datagen.CONFIGS["pubmed"]
+    V, src, dst = datagen.make_graph(cfg)
+    G, og = graph_pair(gsp, V, src, dst)
+    H, F, P = 8, 64, 3
+    Zh = datagen.uniform(1, V, F)
+    wh = datagen.uniform(2, og.E, H, lo=0, hi=1)
+    lh = datagen.uniform(3, og.E, H, lo=-6, hi=6)
+    s_ref, sT = og.gsddmm(Zh, Zh, H)
+    a_ref = og.edge_softmax(lh)
+    w_ref, wT = og.gspmm_weighted(Zh, wh, False)
+    b = G.partition_bounds(P)
+    parts = [G.partition(P, p, device=0) for p in range(P)]
+    R = parts[0].R
+    Zpad = torch.zeros((P * R, F), device="cuda")
+    for p in range(P):
+        Zpad[p * R:p * R + b[p + 1] - b[p]] = dev(Zh[b[p]:b[p + 1]])
+    for p, pg in enumerate(parts):
+        e0, e1 = og.fwd_off[b[p]], og.fwd_off[b[p + 1]]
+        n = b[p + 1] - b[p]
+        assert pg.E == e1 - e0
+        assert_within(pg.gsddmm(Zpad, Zpad, H=H).cpu().numpy(), s_ref[e0:e1], sT[e0:e1], "part gsddmm")
+        assert_within(pg.edge_softmax(dev(lh[e0:e1])).cpu().numpy(), a_ref[e0:e1], 1.0, "part softmax")
+        o = pg.gspmm_weighted(Zpad, dev(wh[e0:e1])).cpu().numpy()
+        assert_within(o[:n], w_ref[b[p]:b[p + 1]], wT[b[p]:b[p + 1]], "part weighted")
+
+
+# ------------------------------------------------------------------ errors
+def test_error_codes(gsp, golden):
+    g = golden("d4.json")
+    G = gsp.Graph(g["V"], g["src"], g["dst"], device=0)
+    X = torch.ones((4, 8), device="cuda")
+    with pytest.raises(gsp.GspError) as ei:
+        G.gspmm(X, 2, out=X)
+    assert ei.value.name == "GSP_ERR_ALIAS"
+    with pytest.raises(gsp.GspError) as ei:
+        G.gspmm(torch.ones((5, 8), device="cuda"), 2)
+    assert ei.value.name == "GSP_ERR_SHAPE"
+    with pytest.raises(gsp.GspError) as ei:
+        G.gspmm(X, 3)
+    assert ei.value.name == "GSP_ERR_ARG"
+    with pytest.raises(gsp.GspError) as ei:
+        G.gspmm(torch.ones((4, 8)), 2, out=torch.empty((4, 8), device="cuda"))   # host tensor
+    assert ei.value.name == "GSP_ERR_ARG"
+    Gnr = gsp.Graph(g["V"], g["src"], g["dst"], device=0, reverse=False)
+    with pytest.raises(gsp.GspError) as ei:
+        Gnr.gspmm(X, 2, reverse=True)
+    assert ei.value.name == "GSP_ERR_NO_REVERSE"
+    e = torch.ones((7, 2), device="cuda")
+    with pytest.raises(gsp.GspError) as ei:
+        G.edge_softmax(e, out=e[1:])
+    assert ei.value.name in ("GSP_ERR_ALIAS", "GSP_ERR_SHAPE")
+    with pytest.raises(gsp.GspError) as ei:
+        G.gspmm_weighted(X, torch.ones((7, 3), device="cuda"))
+    assert ei.value.name == "GSP_ERR_SHAPE"
+    torch.cuda.synchronize()
+
+
+def test_empty_and_degenerate(gsp):
+    G = gsp.Graph(6, np.zeros(0, np.int64), np.zeros(0, np.int64), device=0)
+    X = torch.randn((6, 5), device="cuda")
+    out = torch.full((6, 5), float("nan"), device="cuda")
+    G.gspmm(X, 2, out=out)
+    assert torch.all(out == 0)
+    out.fill_(float("nan"))
+    G.gspmm(X, 2, out=out, reverse=True)
+    assert torch.all(out == 0)
+    # zero-width features, zero heads
+    G.gspmm(torch.empty((6, 0), device="cuda"), 2)
+    torch.cuda.synchronize()
