@@ -90,7 +90,7 @@ __device__ __forceinline__ bool warp_task(const int64_t *off, const int32_t *ord
 // MODE kSpmmWeightedFwd : out[r, h-block] = sum_j w[j, h] * X[col_j, h-block]   (gSpMMve)
 // MODE kSpmmWeightedRev : out[r, h-block] = sum_k w[eid_k, h] * X[col_k, ...]   (gSpMMve^T via eid)
 template <int VEC, int LPE, int CPL, int MODE>
-__global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
+__global__ void __launch_bounds__(kThreads, (CPL <= 2 ? 4 : 2)) spmm_kernel(const SpmmArgs a) {
     constexpr int G = 32 / LPE;
     constexpr int U = CPL >= 3 ? 1 : (CPL == 2 ? 2 : 4);
     constexpr int NACC = U >= 2 ? 2 : 1;
@@ -105,11 +105,14 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
     bool heavy;
     if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
 
-    Vec<VEC> acc[NACC][CPL];
+    // Summation: each 32-edge tile is summed
+    // plainly into `tile` (<= 32/G terms per lane), and tile sums are folded
+    // into a Kahan-compensated running sum (acc, cmp).  The error is then
+    // O(32/G * u) relative to sum|terms|, independent of the row length, so
+    // hub rows of any degree stay far inside 1e-5 * (sum|terms| + 1).
+    Vec<VEC> acc[CPL], cmp[CPL];
 #pragma unroll
-    for (int s = 0; s < NACC; s++)
-#pragma unroll
-        for (int q = 0; q < CPL; q++) vzero(acc[s][q]);
+    for (int q = 0; q < CPL; q++) { vzero(acc[q]); vzero(cmp[q]); }
 
     for (int64_t base = b; base < e; base += 32) {
         const int n = (int)(e - base < 32 ? e - base : 32);
@@ -125,6 +128,11 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
                 ev = __ldg(a.eid + base + lane);
             }
         }
+        Vec<VEC> tile[NACC][CPL];
+#pragma unroll
+        for (int s2 = 0; s2 < NACC; s2++)
+#pragma unroll
+            for (int q = 0; q < CPL; q++) vzero(tile[s2][q]);
         for (int k = 0; k < n; k += G * U) {
             Vec<VEC> x[U][CPL];
             float wt[U][CPL];
@@ -156,19 +164,29 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
                 for (int q = 0; q < CPL; q++)
 #pragma unroll
                     for (int t = 0; t < VEC; t++)
-                        acc[u % NACC][q].v[t] = fmaf(wt[u][q], x[u][q].v[t], acc[u % NACC][q].v[t]);
+                        tile[u % NACC][q].v[t] = fmaf(wt[u][q], x[u][q].v[t], tile[u % NACC][q].v[t]);
         }
+#pragma unroll
+        for (int q = 0; q < CPL; q++)
+#pragma unroll
+            for (int t = 0; t < VEC; t++) {
+                float y = tile[0][q].v[t];
+                if constexpr (NACC == 2) y += tile[1][q].v[t];
+                y -= cmp[q].v[t];
+                const float sum = acc[q].v[t] + y;
+                cmp[q].v[t] = (sum - acc[q].v[t]) - y;
+                acc[q].v[t] = sum;
+            }
     }
-    // combine accumulator sets, then the G edge groups of the warp
+    // compensated totals, then the G edge groups of the warp (xor tree)
 #pragma unroll
     for (int q = 0; q < CPL; q++)
 #pragma unroll
         for (int t = 0; t < VEC; t++) {
-            float v = acc[0][q].v[t];
-            if constexpr (NACC == 2) v += acc[1][q].v[t];
+            float v = acc[q].v[t] - cmp[q].v[t];
 #pragma unroll
             for (int o = LPE; o < 32; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
-            acc[0][q].v[t] = v;
+            acc[q].v[t] = v;
         }
 
     float rs = 1.f;
@@ -183,7 +201,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
                 if (f < a.F) {
                     Vec<VEC> r;
 #pragma unroll
-                    for (int t = 0; t < VEC; t++) r.v[t] = rs * acc[0][q].v[t];
+                    for (int t = 0; t < VEC; t++) r.v[t] = rs * acc[q].v[t];
                     vstore(a.out + row * a.ldo + f, r, a.F - f);
                 }
             }
@@ -195,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
 #pragma unroll
         for (int q = 0; q < CPL; q++)
 #pragma unroll
-            for (int t = 0; t < VEC; t++) red[warp][(sub + q * LPE) * VEC + t] = acc[0][q].v[t];
+            for (int t = 0; t < VEC; t++) red[warp][(sub + q * LPE) * VEC + t] = acc[q].v[t];
     }
     __syncthreads();
     for (int t = threadIdx.x; t < SW; t += kThreads) {

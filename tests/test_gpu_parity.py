@@ -223,10 +223,10 @@ def test_pubmed_gat_chain(gsp):
     G, og = graph_pair(gsp, V, src, dst)
     H, F = cfg.H, cfg.H * cfg.Fh
     Zh = datagen.uniform(1, V, F)
-    ref, T = og.gsddmm(Zh, Zh, H)
+    s_ref, sT = og.gsddmm(Zh, Zh, H)
     Z = dev(Zh)
     s = G.gsddmm(Z, Z, H=H)
-    assert_within(s.cpu().numpy(), ref, T, "pubmed gsddmm")
+    assert_within(s.cpu().numpy(), s_ref, sT, "pubmed gsddmm")
     lh = datagen.uniform(2, og.E, H, lo=-8, hi=8)
     assert_within(G.edge_softmax(dev(lh)).cpu().numpy(), og.edge_softmax(lh), 1.0, "pubmed softmax")
     wh = datagen.uniform(3, og.E, H, lo=0, hi=1)
@@ -237,7 +237,7 @@ def test_pubmed_gat_chain(gsp):
     # tolerance derived in DESIGN.md "Tolerances" (score error x softmax sensitivity)
     a = G.edge_softmax(s)
     out = G.gspmm_weighted(Z, a).cpu().numpy()
-    a_ref = og.edge_softmax(ref.astype(np.float32))
+    a_ref = og.edge_softmax(s_ref.astype(np.float32))
     o_ref, oT = og.gspmm_weighted(Zh, a_ref.astype(np.float32))
     assert_within(out, o_ref, oT, "pubmed chain", scale=1e-3)
 
