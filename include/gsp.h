@@ -137,7 +137,7 @@ gsp_status gsp_gspmm(const gsp_graph *g, const gsp_tensor *X, int norm, gsp_tens
  *  reverse = 0: out[v, h*Fh+f] = sum_{j in fwd row v} w[j, h] * X[col_j, h*Fh+f]
  *  reverse = 1: out[u, h*Fh+f] = sum_{k in rev row u} w[rev_eid_k, h] * X[rcol_k, h*Fh+f]
  * w is [E, H] indexed by edge ID (no eShuffle, no O(E) temporary).
- * Errors as gsp_gspmm; SHAPE also when w->rows != E or X->cols % H != 0.
+ * Errors as gsp_gspmm; SHAPE also when w->rows != E, H > 16 or X->cols % H != 0.
  * Partition graphs: reverse = 0 only (reverse = 1 -> GSP_ERR_NO_REVERSE). */
 gsp_status gsp_gspmm_weighted(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *w,
                               gsp_tensor *out, int reverse, gsp_stream stream);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -215,6 +216,10 @@ static gsp_status upload_full(gsp_graph *g) {
     const gsp::HostGraph &h = g->host;
     DeviceGuard dg(g->device);
     if (!dg.ok) return fail(GSP_ERR_ARG, "cannot select device " + std::to_string(g->device));
+    if (const char *pm = getenv("GSP_L2_PERSIST_MB")) {   // experiment knob
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atol(pm) << 20);
+        cudaGetLastError();
+    }
     gsp_status st;
     std::vector<int64_t> din = degrees_of(h.fwd_off), dout;
     if (h.has_rev) dout = degrees_of(h.rev_off);
@@ -370,7 +375,7 @@ gsp_status gsp_gspmm_weighted(const gsp_graph *g, const gsp_tensor *X, const gsp
     if (!X || !w || !out) return fail(GSP_ERR_NULL, "X/w/out is NULL");
     if ((st = check_tensor(g, w, "w", g->E, -1)) != GSP_OK) return st;
     const int64_t H = w->cols;
-    if (H < 1) return fail(GSP_ERR_SHAPE, "w must have H >= 1 columns");
+    if (H < 1 || H > 16) return fail(GSP_ERR_SHAPE, "w must have 1 <= H <= 16 columns (heads)");
     if ((st = check_tensor(g, X, "X", S.ncols, -1)) != GSP_OK) return st;
     if (X->cols % H != 0) return fail(GSP_ERR_SHAPE, "X.cols must be a multiple of H = w.cols");
     if ((st = check_tensor(g, out, "out", S.nrows, X->cols)) != GSP_OK) return st;

@@ -1,23 +1,30 @@
 // sm_100a kernels of the GraphPy sparse hot path (arxiv 2402.03548).
 //
 // All three families are sparse gather-reduces (no dense contraction), so they
-// run on the LSU/L2 path, not on tensor cores.  Common
+// run on the LSU / L2 path, not on tensor cores.  Common
 // structure:
 //   * rows come from a degree-ordered schedule built at graph create (rows by
-//     descending degree; LPT order): the first n_heavy rows (degree > 1024)
+//     descending degree, LPT order): the first n_heavy rows (degree > 1024)
 //     get a whole CTA (8 warps split the row's edge list, deterministic smem
 //     combine), the rest one warp each (8 rows per CTA);
-//   * a warp reads 32 column ids (and edge ids / scales) with one coalesced
-//     load and broadcasts them with __shfl_sync;
-//   * feature rows are gathered with 128-bit __ldg (read-only path) by groups
-//     of LPE lanes, G = 32/LPE edges at a time, U edges unrolled per lane for
-//     memory-level parallelism; partial sums are combined by xor-shuffles.
+//   * a warp walks its edge list in 32-edge tiles: one coalesced load of 32
+//     column ids (+ the per-edge scale / edge-ID-indirected weight row), staged
+//     in shared memory so that each lane group fetches (col, weight) pairs with
+//     one 128-bit LDS per two edges;
+//   * feature rows are gathered by groups of LPE lanes, G = 32/LPE edges per
+//     warp instruction, with 256-bit (LDG.E.256, sm_100) or 128-bit loads and
+//     an L2 evict_last policy (the gathered table is the reused operand);
+//     index / edge-value streams use L1::no_allocate + L2 evict_first so they
+//     do not push the table out of L2;
+//   * fp32 accumulation: plain sums over <= 128-edge chunks folded into a
+//     Kahan-compensated running sum (error independent of row length).
 // No atomics; every output element is written exactly once per call.
 #include <cuda_runtime.h>
 
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -27,33 +34,96 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kHMax = 16;        // weighted modes stage w rows of <= kHMax heads in smem
+constexpr int kFoldTiles = 4;    // 32-edge tiles summed plainly before a Kahan fold
 
 template <int VEC>
 struct Vec {
     float v[VEC];
 };
 
+// ------------------------------------------------------- memory primitives
+struct Pol {
+    uint64_t keep, stream;
+};
+__device__ __forceinline__ Pol make_pol() {
+    Pol p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p.keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p.stream));
+    return p;
+}
+
+// gathered feature rows: read-only path, L2 evict_last
 template <int VEC>
-__device__ __forceinline__ void vload(Vec<VEC> &r, const float *p) {
-    if constexpr (VEC == 4) {
-        float4 t = __ldg(reinterpret_cast<const float4 *>(p));
-        r.v[0] = t.x; r.v[1] = t.y; r.v[2] = t.z; r.v[3] = t.w;
+__device__ __forceinline__ void ld_keep(Vec<VEC> &r, const float *p, uint64_t pol) {
+    if constexpr (VEC == 8) {
+        unsigned u0, u1, u2, u3, u4, u5, u6, u7;
+        asm volatile("ld.global.nc.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                     : "=r"(u0), "=r"(u1), "=r"(u2), "=r"(u3), "=r"(u4), "=r"(u5), "=r"(u6), "=r"(u7)
+                     : "l"(p), "l"(pol));
+        r.v[0] = __uint_as_float(u0); r.v[1] = __uint_as_float(u1);
+        r.v[2] = __uint_as_float(u2); r.v[3] = __uint_as_float(u3);
+        r.v[4] = __uint_as_float(u4); r.v[5] = __uint_as_float(u5);
+        r.v[6] = __uint_as_float(u6); r.v[7] = __uint_as_float(u7);
+    } else if constexpr (VEC == 4) {
+        asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                     : "l"(p), "l"(pol));
     } else {
-#pragma unroll
-        for (int k = 0; k < VEC; k++) r.v[k] = __ldg(p + k);
+        asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r.v[0]) : "l"(p), "l"(pol));
     }
 }
+// streamed once: no L1 allocation, L2 evict_first
+__device__ __forceinline__ int ld_stream_i32(const int32_t *p, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_stream_f32(const float *p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float4 ld_stream_f4(const float *p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+// plain (coherent) loads of data the caller may alias with the output (softmax in place)
+__device__ __forceinline__ float4 ld_f4(const float *p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_f32(const float *p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_stream_f32(float *p, float v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_stream_f4(float *p, float4 v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
+                 "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
+}
+
 template <int VEC>
 __device__ __forceinline__ void vzero(Vec<VEC> &r) {
 #pragma unroll
     for (int k = 0; k < VEC; k++) r.v[k] = 0.f;
 }
-// store the first `lim` (<= VEC) elements; full vector store when lim == VEC
+// store the first `lim` (<= VEC) elements; vector stores when lim == VEC
 template <int VEC>
 __device__ __forceinline__ void vstore(float *p, const Vec<VEC> &r, int64_t lim) {
-    if constexpr (VEC == 4) {
-        if (lim >= 4) {
-            *reinterpret_cast<float4 *>(p) = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
+    if constexpr (VEC >= 4) {
+        if (lim >= VEC) {
+#pragma unroll
+            for (int k = 0; k < VEC; k += 4)
+                *reinterpret_cast<float4 *>(p + k) = make_float4(r.v[k], r.v[k + 1], r.v[k + 2], r.v[k + 3]);
             return;
         }
     }
@@ -89,13 +159,19 @@ __device__ __forceinline__ bool warp_task(const int64_t *off, const int32_t *ord
 // MODE kSpmmScaled      : out[r] = rs(r) * sum_j cs(col_j) * X[col_j]          (gSpMMv + norm)
 // MODE kSpmmWeightedFwd : out[r, h-block] = sum_j w[j, h] * X[col_j, h-block]   (gSpMMve)
 // MODE kSpmmWeightedRev : out[r, h-block] = sum_k w[eid_k, h] * X[col_k, ...]   (gSpMMve^T via eid)
-template <int VEC, int LPE, int CPL, int MODE>
-__global__ void __launch_bounds__(kThreads, (CPL <= 2 ? 4 : 2)) spmm_kernel(const SpmmArgs a) {
-    constexpr int G = 32 / LPE;
-    constexpr int U = CPL >= 3 ? 1 : (CPL == 2 ? 2 : 4);
-    constexpr int NACC = U >= 2 ? 2 : 1;
-    constexpr int SW = VEC * LPE * CPL;  // feature slab handled by this CTA
-    __shared__ float red[kWarps][SW];
+template <int VEC, int LPE, int CPL, int MODE, bool HAS_CS, int UOVR = 0, int MINB = 0>
+__global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 : 2))) spmm_kernel(const SpmmArgs a) {
+    constexpr int G = 32 / LPE;           // edge groups per warp
+    constexpr int PER = LPE;              // edges per group per 32-edge tile
+    constexpr int UB = 32 / (VEC * CPL);  // loads in flight per lane: ~32 floats
+    constexpr int U0 = UOVR ? UOVR : (UB < 2 ? 2 : (UB > 4 ? 4 : UB));
+    constexpr int U = U0 > PER ? PER : U0;
+    constexpr int SW = VEC * LPE * CPL;   // feature slab handled by this CTA
+    constexpr bool W = MODE != kSpmmScaled;
+    constexpr int RED = kWarps * SW;
+    constexpr int WS = W ? kWarps * 32 * kHMax : 0;
+    __shared__ __align__(16) int2 s_pair[kWarps][32];
+    __shared__ __align__(16) float s_raw[RED > WS ? RED : WS];   // weights during the walk, then heavy combine
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / LPE, sub = lane % LPE;
@@ -104,57 +180,88 @@ __global__ void __launch_bounds__(kThreads, (CPL <= 2 ? 4 : 2)) spmm_kernel(cons
     int64_t row, b, e;
     bool heavy;
     if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    const Pol pol = make_pol();
 
-    // Summation: each 32-edge tile is summed
-    // plainly into `tile` (<= 32/G terms per lane), and tile sums are folded
-    // into a Kahan-compensated running sum (acc, cmp).  The error is then
-    // O(32/G * u) relative to sum|terms|, independent of the row length, so
-    // hub rows of any degree stay far inside 1e-5 * (sum|terms| + 1).
-    Vec<VEC> acc[CPL], cmp[CPL];
+    // lane constants: feature chunk q covers [f, f + VEC) of head hq
+    const char *xl[CPL];
+    bool fv[CPL];
+    int hq[CPL];
 #pragma unroll
-    for (int q = 0; q < CPL; q++) { vzero(acc[q]); vzero(cmp[q]); }
+    for (int q = 0; q < CPL; q++) {
+        const int64_t f = f0 + (int64_t)(sub + q * LPE) * VEC;
+        fv[q] = f < a.F;
+        xl[q] = reinterpret_cast<const char *>(a.X + (fv[q] ? f : 0));
+        hq[q] = W ? (int)((fv[q] ? f : 0) / a.Fh) : 0;
+    }
+    const uint32_t ldxb = (uint32_t)(a.ldx * 4);
+    const int H = W ? (int)a.H : 0;
+    float *s_w = s_raw + warp * 32 * kHMax;
+
+    // Summation: <= kFoldTiles*32/G terms per
+    // lane summed plainly into `tile`, then folded into a Kahan-compensated
+    // running sum (acc, cmp): error O((128/G) u) relative to sum|terms|,
+    // independent of the row length.
+    constexpr int NT = VEC >= 4 ? 1 : 2;   // independent tile accumulators (ILP for narrow lanes)
+    Vec<VEC> acc[CPL], cmp[CPL], tile[NT][CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; q++) {
+        vzero(acc[q]); vzero(cmp[q]);
+#pragma unroll
+        for (int k = 0; k < NT; k++) vzero(tile[k][q]);
+    }
+    int ntile = 0;
 
     for (int64_t base = b; base < e; base += 32) {
         const int n = (int)(e - base < 32 ? e - base : 32);
+        // ---- stage this tile's (col, weight) pairs (and weight rows) in smem
         int c = 0, ev = 0;
-        float sc = 1.f;
+        float wv = 0.f;
         if (lane < n) {
-            c = __ldg(a.col + base + lane);
-            if constexpr (MODE == kSpmmScaled) {
-                if (a.col_scale) sc = __ldg(a.col_scale + c);
-            } else if constexpr (MODE == kSpmmWeightedFwd) {
-                ev = (int)(base + lane);
+            c = ld_stream_i32(a.col + base + lane, pol.stream);
+            if constexpr (MODE == kSpmmScaled) wv = HAS_CS ? __ldg(a.col_scale + c) : 1.f;
+            else if constexpr (MODE == kSpmmWeightedFwd) ev = (int)(base + lane);
+            else ev = ld_stream_i32(a.eid + base + lane, pol.stream);
+        }
+        const int slot = (lane % G) * PER + lane / G;   // group-contiguous layout
+        s_pair[warp][slot] = make_int2(c, __float_as_int(wv));
+        if constexpr (W) {
+            const float *wr = a.w + (int64_t)ev * a.ldw;
+            float *dst = s_w + slot * H;
+            if (H == 8 && a.ldw == 8) {
+                float4 w0 = make_float4(0.f, 0.f, 0.f, 0.f), w1 = w0;
+                if (lane < n) { w0 = ld_stream_f4(wr, pol.stream); w1 = ld_stream_f4(wr + 4, pol.stream); }
+                reinterpret_cast<float4 *>(dst)[0] = w0;
+                reinterpret_cast<float4 *>(dst)[1] = w1;
             } else {
-                ev = __ldg(a.eid + base + lane);
+                for (int t = 0; t < H; t++) dst[t] = lane < n ? ld_stream_f32(wr + t, pol.stream) : 0.f;
             }
         }
-        Vec<VEC> tile[NACC][CPL];
-#pragma unroll
-        for (int s2 = 0; s2 < NACC; s2++)
-#pragma unroll
-            for (int q = 0; q < CPL; q++) vzero(tile[s2][q]);
-        for (int k = 0; k < n; k += G * U) {
+        __syncwarp();
+        const int2 *gp = &s_pair[warp][g * PER];
+        const float *gw = s_w + g * PER * H;
+
+        auto body = [&](int i, bool full, int m) {
             Vec<VEC> x[U][CPL];
             float wt[U][CPL];
 #pragma unroll
-            for (int u = 0; u < U; u++) {
-                const int ei = k + u * G + g;
-                const bool ok = ei < n;
-                const int cu = __shfl_sync(kFull, c, ei & 31);
-                float su = 1.f;
-                int eu = 0;
-                if constexpr (MODE == kSpmmScaled) su = __shfl_sync(kFull, sc, ei & 31);
-                else eu = __shfl_sync(kFull, ev, ei & 31);
+            for (int u = 0; u < U; u += 2) {
+                const int4 pp = *reinterpret_cast<const int4 *>(gp + i + u);
+                const int cc[2] = {pp.x, pp.z};
+                const float ww[2] = {__int_as_float(pp.y), __int_as_float(pp.w)};
 #pragma unroll
-                for (int q = 0; q < CPL; q++) {
-                    const int64_t f = f0 + (int64_t)(sub + q * LPE) * VEC;
-                    if (ok && f < a.F) {
-                        vload(x[u][q], a.X + (int64_t)cu * a.ldx + f);
-                        if constexpr (MODE == kSpmmScaled) wt[u][q] = su;
-                        else wt[u][q] = __ldg(a.w + (int64_t)eu * a.ldw + f / a.Fh);
-                    } else {
-                        vzero(x[u][q]);
-                        wt[u][q] = 0.f;
+                for (int k = 0; k < 2; k++) {
+                    const bool ok = full || (i + u + k < m);
+#pragma unroll
+                    for (int q = 0; q < CPL; q++) {
+                        if (ok && fv[q]) {
+                            ld_keep(x[u + k][q],
+                                    reinterpret_cast<const float *>(xl[q] + (uint64_t)(uint32_t)cc[k] * ldxb),
+                                    pol.keep);
+                        } else {
+                            vzero(x[u + k][q]);
+                        }
+                        if constexpr (W) wt[u + k][q] = gw[(i + u + k) * H + hq[q]];
+                        else wt[u + k][q] = ww[k];
                     }
                 }
             }
@@ -164,19 +271,33 @@ __global__ void __launch_bounds__(kThreads, (CPL <= 2 ? 4 : 2)) spmm_kernel(cons
                 for (int q = 0; q < CPL; q++)
 #pragma unroll
                     for (int t = 0; t < VEC; t++)
-                        tile[u % NACC][q].v[t] = fmaf(wt[u][q], x[u][q].v[t], tile[u % NACC][q].v[t]);
+                        tile[u % NT][q].v[t] = fmaf(wt[u][q], x[u][q].v[t], tile[u % NT][q].v[t]);
+        };
+        if (n == 32) {
+#pragma unroll 1
+            for (int i = 0; i < PER; i += U) body(i, true, PER);
+        } else {
+            const int m = n > g ? (n - g + G - 1) / G : 0;
+#pragma unroll 1
+            for (int i = 0; i < m; i += U) body(i, false, m);
         }
+        __syncwarp();
+        if (++ntile == kFoldTiles || base + 32 >= e) {
+            ntile = 0;
 #pragma unroll
-        for (int q = 0; q < CPL; q++)
+            for (int q = 0; q < CPL; q++)
 #pragma unroll
-            for (int t = 0; t < VEC; t++) {
-                float y = tile[0][q].v[t];
-                if constexpr (NACC == 2) y += tile[1][q].v[t];
-                y -= cmp[q].v[t];
-                const float sum = acc[q].v[t] + y;
-                cmp[q].v[t] = (sum - acc[q].v[t]) - y;
-                acc[q].v[t] = sum;
-            }
+                for (int t = 0; t < VEC; t++) {
+                    float y = tile[0][q].v[t];
+                    if constexpr (NT == 2) y += tile[1][q].v[t];
+                    y -= cmp[q].v[t];
+                    const float sum = acc[q].v[t] + y;
+                    cmp[q].v[t] = (sum - acc[q].v[t]) - y;
+                    acc[q].v[t] = sum;
+#pragma unroll
+                    for (int k = 0; k < NT; k++) tile[k][q].v[t] = 0.f;
+                }
+        }
     }
     // compensated totals, then the G edge groups of the warp (xor tree)
 #pragma unroll
@@ -209,11 +330,13 @@ __global__ void __launch_bounds__(kThreads, (CPL <= 2 ? 4 : 2)) spmm_kernel(cons
         return;
     }
     // heavy row: deterministic cross-warp combine in warp order
+    float *red = s_raw;
+    __syncthreads();   // every warp is done with its s_w slice (aliased by red)
     if (g == 0) {
 #pragma unroll
         for (int q = 0; q < CPL; q++)
 #pragma unroll
-            for (int t = 0; t < VEC; t++) red[warp][(sub + q * LPE) * VEC + t] = acc[q].v[t];
+            for (int t = 0; t < VEC; t++) red[warp * SW + (sub + q * LPE) * VEC + t] = acc[q].v[t];
     }
     __syncthreads();
     for (int t = threadIdx.x; t < SW; t += kThreads) {
@@ -221,19 +344,23 @@ __global__ void __launch_bounds__(kThreads, (CPL <= 2 ? 4 : 2)) spmm_kernel(cons
         if (f < a.F) {
             float v = 0.f;
 #pragma unroll
-            for (int w = 0; w < kWarps; w++) v += red[w][t];
+            for (int w = 0; w < kWarps; w++) v += red[w * SW + t];
             a.out[row * a.ldo + f] = rs * v;
         }
     }
 }
 
 // ================================================================ gSDDMMvv
-// out[j, h] = <X[row_base + v, head h], Y[col_j, head h]>, CPH = Fh / VEC lanes per head.
+// out[j, h] = <X[row_base + v, head h], Y[col_j, head h]>; CPH = Fh / VEC lanes per head.
 template <int VEC, int LPE, int CPL, int CPH>
-__global__ void __launch_bounds__(kThreads) sddmm_kernel(const SddmmArgs a) {
+__global__ void __launch_bounds__(kThreads, (VEC * CPL <= 8 ? 3 : 2)) sddmm_kernel(const SddmmArgs a) {
     constexpr int G = 32 / LPE;
-    constexpr int U = CPL >= 3 ? 1 : (CPL == 2 ? 2 : 4);
+    constexpr int PER = LPE;
+    constexpr int UB = 32 / (VEC * CPL);
+    constexpr int U0 = UB < 2 ? 2 : (UB > 4 ? 4 : UB);
+    constexpr int U = U0 > PER ? PER : U0;
     constexpr int SW = VEC * LPE * CPL;
+    __shared__ __align__(16) int s_col[kWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / LPE, sub = lane % LPE;
     const int64_t F = a.H * a.Fh;
@@ -243,36 +370,57 @@ __global__ void __launch_bounds__(kThreads) sddmm_kernel(const SddmmArgs a) {
     bool heavy;
     if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     if (b >= e) return;
+    const Pol pol = make_pol();
 
-    // the row's features are fetched once and reused for every edge (P:2041-2042)
+    const char *yl[CPL];
+    bool fv[CPL], wr[CPL];
+    int hq[CPL];
     Vec<VEC> xv[CPL];
+    // the row's features are fetched once and reused for every edge (P:2041-2042)
     const float *xr = a.X + (a.row_base + row) * a.ldx;
 #pragma unroll
     for (int q = 0; q < CPL; q++) {
         const int64_t f = f0 + (int64_t)(sub + q * LPE) * VEC;
-        if (f < F) vload(xv[q], xr + f);
+        fv[q] = f < F;
+        yl[q] = reinterpret_cast<const char *>(a.Y + (fv[q] ? f : 0));
+        hq[q] = (int)((fv[q] ? f : 0) / a.Fh);
+        wr[q] = fv[q] && (sub % CPH) == 0;
+        if (fv[q]) ld_keep(xv[q], xr + f, pol.stream);
         else vzero(xv[q]);
     }
+    const uint32_t ldyb = (uint32_t)(a.ldy * 4);
+
     for (int64_t base = b; base < e; base += 32) {
         const int n = (int)(e - base < 32 ? e - base : 32);
         int c = 0;
-        if (lane < n) c = __ldg(a.col + base + lane);
-        for (int k = 0; k < n; k += G * U) {
+        if (lane < n) c = ld_stream_i32(a.col + base + lane, pol.stream);
+        s_col[warp][(lane % G) * PER + lane / G] = c;
+        __syncwarp();
+        const int *gp = &s_col[warp][g * PER];
+        float *ob = a.out + (base + g) * a.ldo;   // group g's i-th edge is tile edge g + G*i
+
+        auto body = [&](int i, bool full, int m) {
             Vec<VEC> y[U][CPL];
 #pragma unroll
-            for (int u = 0; u < U; u++) {
-                const int ei = k + u * G + g;
-                const int cu = __shfl_sync(kFull, c, ei & 31);
+            for (int u = 0; u < U; u += 2) {
+                const int2 cc = *reinterpret_cast<const int2 *>(gp + i + u);
+                const int c2[2] = {cc.x, cc.y};
 #pragma unroll
-                for (int q = 0; q < CPL; q++) {
-                    const int64_t f = f0 + (int64_t)(sub + q * LPE) * VEC;
-                    if (ei < n && f < F) vload(y[u][q], a.Y + (int64_t)cu * a.ldy + f);
-                    else vzero(y[u][q]);
+                for (int k = 0; k < 2; k++) {
+                    const bool ok = full || (i + u + k < m);
+#pragma unroll
+                    for (int q = 0; q < CPL; q++) {
+                        if (ok && fv[q])
+                            ld_keep(y[u + k][q],
+                                    reinterpret_cast<const float *>(yl[q] + (uint64_t)(uint32_t)c2[k] * ldyb),
+                                    pol.keep);
+                        else vzero(y[u + k][q]);
+                    }
                 }
             }
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const int ei = k + u * G + g;
+                const bool ok = full || (i + u < m);
 #pragma unroll
                 for (int q = 0; q < CPL; q++) {
                     float p = 0.f;
@@ -280,12 +428,21 @@ __global__ void __launch_bounds__(kThreads) sddmm_kernel(const SddmmArgs a) {
                     for (int t = 0; t < VEC; t++) p = fmaf(xv[q].v[t], y[u][q].v[t], p);
 #pragma unroll
                     for (int o = 1; o < CPH; o <<= 1) p += __shfl_xor_sync(kFull, p, o);
-                    const int64_t f = f0 + (int64_t)(sub + q * LPE) * VEC;
-                    if (ei < n && (sub % CPH) == 0 && f < F)
-                        a.out[(base + ei) * a.ldo + f / a.Fh] = p;
+                    if (ok && wr[q]) st_stream_f32(ob + (int64_t)(G * (i + u)) * a.ldo + hq[q], p, pol.stream);
                 }
             }
+        };
+        if (n == 32) {
+#pragma unroll 1
+            for (int i = 0; i < PER; i += U) body(i, true, PER);
+        } else {
+            const int m = n > g ? (n - g + G - 1) / G : 0;
+            // all lanes run the same trip count (the xor-shuffles need the full warp)
+            const int mmax = (n + G - 1) / G;
+#pragma unroll 1
+            for (int i = 0; i < mmax; i += U) body(i, false, m);
         }
+        __syncwarp();
     }
 }
 
@@ -325,10 +482,23 @@ __device__ __forceinline__ void online_merge(float &m, float &s, float mo, float
     s = a + b;
 }
 
-// Fast path: e, out contiguous [E, H] (ld == H), H divides 32*VEC/ (so every
-// lane always sees the same VEC heads).  HPL = H / VEC lanes per head period.
+// exp(x) for x <= 0 via ex2.approx: relative error ~2^-22 + |x| 2^-24 (x is a
+// logit difference, |x| <~ 100), far inside the 2e-5 absolute bound on alpha.
+__device__ __forceinline__ float fast_exp(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
+    return y;
+}
+
+// Fast path: e, out contiguous [E, H] (ld == H) with H | 32*VEC, so every lane
+// always sees the same VEC heads; HPL = H / VEC lanes per head period.  Pass 1
+// keeps a running (max, sum) per head, updated once per batch of UNR values
+// (one rescale per batch); pass 2 re-reads the row block (L2-resident: pass 1
+// loads use evict_last) and streams alpha = exp(x - m) * (1/s) out.
 template <int VEC>
 __global__ void __launch_bounds__(kThreads) softmax_kernel(const SoftmaxArgs a) {
+    constexpr int UNR = 4;
+    constexpr int STEP = 32 * VEC;
     __shared__ float sm_m[kWarps][32];
     __shared__ float sm_s[kWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -337,23 +507,53 @@ __global__ void __launch_bounds__(kThreads) softmax_kernel(const SoftmaxArgs a) 
     int64_t row, b, e;
     bool heavy;
     if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    const Pol pol = make_pol();
 
     float m[VEC], s[VEC];
 #pragma unroll
     for (int t = 0; t < VEC; t++) { m[t] = -INFINITY; s[t] = 0.f; }
     const int64_t lo = b * H, hi = e * H;
-    for (int64_t i = lo + (int64_t)lane * VEC; i < hi; i += 32 * VEC) {
-        Vec<VEC> x;
-        vload(x, a.e + i);
+    for (int64_t i0 = lo + (int64_t)lane * VEC; i0 < hi; i0 += STEP * UNR) {
+        float x[UNR][VEC];
 #pragma unroll
-        for (int t = 0; t < VEC; t++) online_push(m[t], s[t], x.v[t]);
+        for (int k = 0; k < UNR; k++) {
+            const int64_t i = i0 + (int64_t)k * STEP;
+            if (i < hi) {
+                if constexpr (VEC == 4) {
+                    const float4 v = ld_f4(a.e + i, pol.keep);
+                    x[k][0] = v.x; x[k][1] = v.y; x[k][2] = v.z; x[k][3] = v.w;
+                } else {
+                    x[k][0] = ld_f32(a.e + i, pol.keep);
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < VEC; t++) x[k][t] = -INFINITY;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < VEC; t++) {
+            float mb = x[0][t];
+#pragma unroll
+            for (int k = 1; k < UNR; k++) mb = fmaxf(mb, x[k][t]);
+            const float mn = fmaxf(m[t], mb);            // finite: x[0] is always in range
+            float acc = (m[t] == -INFINITY) ? 0.f : s[t] * fast_exp(m[t] - mn);
+#pragma unroll
+            for (int k = 0; k < UNR; k++) acc += fast_exp(x[k][t] - mn);   // exp(-inf) = 0 for padding
+            m[t] = mn;
+            s[t] = acc;
+        }
     }
 #pragma unroll
     for (int t = 0; t < VEC; t++)
         for (int o = HPL; o < 32; o <<= 1) {
             const float mo = __shfl_xor_sync(kFull, m[t], o);
             const float so = __shfl_xor_sync(kFull, s[t], o);
-            online_merge(m[t], s[t], mo, so);
+            const float mn = fmaxf(m[t], mo);
+            if (mn != -INFINITY) {
+                s[t] = ((m[t] == -INFINITY) ? 0.f : s[t] * fast_exp(m[t] - mn)) +
+                       ((mo == -INFINITY) ? 0.f : so * fast_exp(mo - mn));
+                m[t] = mn;
+            }
         }
     if (heavy) {
         // lanes 0..HPL-1 hold heads lane*VEC + t; combine across warps in order
@@ -369,17 +569,47 @@ __global__ void __launch_bounds__(kThreads) softmax_kernel(const SoftmaxArgs a) 
 #pragma unroll
         for (int t = 0; t < VEC; t++) {
             float mm = -INFINITY, ss = 0.f;
-            for (int w = 0; w < kWarps; w++) online_merge(mm, ss, sm_m[w][hl * VEC + t], sm_s[w][hl * VEC + t]);
+            for (int w = 0; w < kWarps; w++) {
+                const float mo = sm_m[w][hl * VEC + t], so = sm_s[w][hl * VEC + t];
+                const float mn = fmaxf(mm, mo);
+                if (mn == -INFINITY) continue;
+                ss = ((mm == -INFINITY) ? 0.f : ss * fast_exp(mm - mn)) + ((mo == -INFINITY) ? 0.f : so * fast_exp(mo - mn));
+                mm = mn;
+            }
             m[t] = mm;
             s[t] = ss;
         }
     }
-    for (int64_t i = lo + (int64_t)lane * VEC; i < hi; i += 32 * VEC) {
-        Vec<VEC> x, r;
-        vload(x, a.e + i);
+    float rinv[VEC];
 #pragma unroll
-        for (int t = 0; t < VEC; t++) r.v[t] = expf(x.v[t] - m[t]) / s[t];
-        vstore(a.out + i, r, VEC);
+    for (int t = 0; t < VEC; t++) rinv[t] = 1.0f / s[t];
+    for (int64_t i0 = lo + (int64_t)lane * VEC; i0 < hi; i0 += STEP * UNR) {
+        float x[UNR][VEC];
+#pragma unroll
+        for (int k = 0; k < UNR; k++) {
+            const int64_t i = i0 + (int64_t)k * STEP;
+            if (i < hi) {
+                if constexpr (VEC == 4) {
+                    const float4 v = ld_f4(a.e + i, pol.stream);
+                    x[k][0] = v.x; x[k][1] = v.y; x[k][2] = v.z; x[k][3] = v.w;
+                } else {
+                    x[k][0] = ld_f32(a.e + i, pol.stream);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; k++) {
+            const int64_t i = i0 + (int64_t)k * STEP;
+            if (i < hi) {
+                if constexpr (VEC == 4) {
+                    st_stream_f4(a.out + i, make_float4(fast_exp(x[k][0] - m[0]) * rinv[0], fast_exp(x[k][1] - m[1]) * rinv[1],
+                                                        fast_exp(x[k][2] - m[2]) * rinv[2], fast_exp(x[k][3] - m[3]) * rinv[3]),
+                                 pol.stream);
+                } else {
+                    st_stream_f32(a.out + i, fast_exp(x[k][0] - m[0]) * rinv[0], pol.stream);
+                }
+            }
+        }
     }
 }
 
@@ -408,7 +638,7 @@ __global__ void degree_scales_kernel(const int64_t *deg, int64_t n, float *inv, 
 }
 
 // ---------------------------------------------------------------- dispatch
-inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool aligned(const void *p, unsigned bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
 inline int pow2ceil(int64_t x) {
     int p = 1;
     while (p < x) p <<= 1;
@@ -420,49 +650,83 @@ inline dim3 row_grid(int64_t nrows, int64_t n_heavy, int64_t slabs) {
     return dim3((unsigned)(n_heavy + ceil_div(nrows - n_heavy, kWarps)), (unsigned)slabs, 1);
 }
 
-template <int VEC, int LPE, int CPL>
-cudaError_t spmm_go(const SpmmArgs &a, int mode, int64_t slabs, cudaStream_t s) {
-    dim3 grid = row_grid(a.nrows, a.n_heavy, slabs);
-    if (mode == kSpmmScaled) spmm_kernel<VEC, LPE, CPL, kSpmmScaled><<<grid, kThreads, 0, s>>>(a);
-    else if (mode == kSpmmWeightedFwd) spmm_kernel<VEC, LPE, CPL, kSpmmWeightedFwd><<<grid, kThreads, 0, s>>>(a);
-    else spmm_kernel<VEC, LPE, CPL, kSpmmWeightedRev><<<grid, kThreads, 0, s>>>(a);
+template <int VEC, int LPE, int CPL, int UOVR = 0, int MINB = 0>
+cudaError_t spmm_go_v(const SpmmArgs &a, int mode, int64_t slabs, cudaStream_t s) {
+    const dim3 grid = row_grid(a.nrows, a.n_heavy, slabs);
+    if (mode == kSpmmScaled) {
+        if (a.col_scale) spmm_kernel<VEC, LPE, CPL, kSpmmScaled, true, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
+        else spmm_kernel<VEC, LPE, CPL, kSpmmScaled, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
+    } else if (mode == kSpmmWeightedFwd) {
+        spmm_kernel<VEC, LPE, CPL, kSpmmWeightedFwd, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
+    } else {
+        spmm_kernel<VEC, LPE, CPL, kSpmmWeightedRev, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
+    }
     return cudaGetLastError();
 }
 
-template <int VEC>
+// tuning knob for the hot shape (VEC 8, LPE 8: F = 64): GSP_TUNE_SPMM selects
+// (U, min blocks/SM); read once.  0 = default.
+int tune_spmm() {
+    static int v = [] {
+        const char *e = getenv("GSP_TUNE_SPMM");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
+template <int VEC, int LPE, int CPL>
+cudaError_t spmm_go(const SpmmArgs &a, int mode, int64_t slabs, cudaStream_t s) {
+    if constexpr (VEC == 8 && LPE == 8 && CPL == 1) {
+        switch (tune_spmm()) {
+            case 0:   // measured best on B200 (Reddit-shaped F = 64, tools/opbench.py)
+                if (mode == kSpmmScaled) return spmm_go_v<VEC, LPE, CPL, 8, 3>(a, mode, slabs, s);
+                return spmm_go_v<VEC, LPE, CPL, 2, 4>(a, mode, slabs, s);
+            case 5: return spmm_go_v<VEC, LPE, CPL>(a, mode, slabs, s);
+            case 1: return spmm_go_v<VEC, LPE, CPL, 8, 2>(a, mode, slabs, s);
+            case 2: return spmm_go_v<VEC, LPE, CPL, 4, 4>(a, mode, slabs, s);
+            case 3: return spmm_go_v<VEC, LPE, CPL, 2, 4>(a, mode, slabs, s);
+            case 4: return spmm_go_v<VEC, LPE, CPL, 8, 3>(a, mode, slabs, s);
+            default: break;
+        }
+    }
+    return spmm_go_v<VEC, LPE, CPL>(a, mode, slabs, s);
+}
+
+template <int VEC, int MAXCPL>
 cudaError_t spmm_dispatch(const SpmmArgs &a, int mode, cudaStream_t s) {
     const int64_t nch = ceil_div(a.F, VEC);
     if (nch <= 16) {
-        const int lpe = pow2ceil(nch < 4 ? 4 : nch);
+        const int lpe = pow2ceil(nch < 2 ? 2 : nch);
+        if (lpe == 2) return spmm_go<VEC, 2, 1>(a, mode, 1, s);
         if (lpe == 4) return spmm_go<VEC, 4, 1>(a, mode, 1, s);
         if (lpe == 8) return spmm_go<VEC, 8, 1>(a, mode, 1, s);
         return spmm_go<VEC, 16, 1>(a, mode, 1, s);
     }
-    const int64_t cpl_need = ceil_div(nch, 32);
-    if (cpl_need <= 8) {
-        switch (cpl_need) {
-            case 1: return spmm_go<VEC, 32, 1>(a, mode, 1, s);
-            case 2: return spmm_go<VEC, 32, 2>(a, mode, 1, s);
-            case 3: return spmm_go<VEC, 32, 3>(a, mode, 1, s);
-            case 4: return spmm_go<VEC, 32, 4>(a, mode, 1, s);
-            case 5: return spmm_go<VEC, 32, 5>(a, mode, 1, s);
-            case 6: return spmm_go<VEC, 32, 6>(a, mode, 1, s);
-            case 7: return spmm_go<VEC, 32, 7>(a, mode, 1, s);
-            default: return spmm_go<VEC, 32, 8>(a, mode, 1, s);
-        }
+    // wide rows: balanced feature slabs of <= 32*MAXCPL chunks (VEC*CPL <= 16
+    // floats of state per lane and chunk keeps the kernel spill-free)
+    const int64_t slabs = ceil_div(nch, 32 * MAXCPL);
+    const int64_t cpl = ceil_div(nch, 32 * slabs);
+    switch (cpl) {
+        case 1: return spmm_go<VEC, 32, 1>(a, mode, slabs, s);
+        case 2: return spmm_go<VEC, 32, (MAXCPL >= 2 ? 2 : MAXCPL)>(a, mode, slabs, s);
+        case 3: return spmm_go<VEC, 32, (MAXCPL >= 3 ? 3 : MAXCPL)>(a, mode, slabs, s);
+        case 4: return spmm_go<VEC, 32, (MAXCPL >= 4 ? 4 : MAXCPL)>(a, mode, slabs, s);
+        case 5: return spmm_go<VEC, 32, (MAXCPL >= 5 ? 5 : MAXCPL)>(a, mode, slabs, s);
+        case 6: return spmm_go<VEC, 32, (MAXCPL >= 6 ? 6 : MAXCPL)>(a, mode, slabs, s);
+        case 7: return spmm_go<VEC, 32, (MAXCPL >= 7 ? 7 : MAXCPL)>(a, mode, slabs, s);
+        default: return spmm_go<VEC, 32, MAXCPL>(a, mode, slabs, s);
     }
-    return spmm_go<VEC, 32, 8>(a, mode, ceil_div(nch, 32 * 8), s);
 }
 
 template <int VEC, int LPE, int CPL>
 cudaError_t sddmm_go_cph(const SddmmArgs &a, int cph, int64_t slabs, cudaStream_t s) {
-    dim3 grid = row_grid(a.nrows, a.n_heavy, slabs);
+    const dim3 grid = row_grid(a.nrows, a.n_heavy, slabs);
     switch (cph) {
         case 1: sddmm_kernel<VEC, LPE, CPL, 1><<<grid, kThreads, 0, s>>>(a); break;
-        case 2: if (LPE >= 2) sddmm_kernel<VEC, LPE, CPL, 2><<<grid, kThreads, 0, s>>>(a); break;
-        case 4: if (LPE >= 4) sddmm_kernel<VEC, LPE, CPL, 4><<<grid, kThreads, 0, s>>>(a); break;
-        case 8: if (LPE >= 8) sddmm_kernel<VEC, LPE, CPL, 8><<<grid, kThreads, 0, s>>>(a); break;
-        case 16: if (LPE >= 16) sddmm_kernel<VEC, LPE, CPL, 16><<<grid, kThreads, 0, s>>>(a); break;
+        case 2: sddmm_kernel<VEC, LPE, CPL, (LPE >= 2 ? 2 : 1)><<<grid, kThreads, 0, s>>>(a); break;
+        case 4: sddmm_kernel<VEC, LPE, CPL, (LPE >= 4 ? 4 : 1)><<<grid, kThreads, 0, s>>>(a); break;
+        case 8: sddmm_kernel<VEC, LPE, CPL, (LPE >= 8 ? 8 : 1)><<<grid, kThreads, 0, s>>>(a); break;
+        case 16: sddmm_kernel<VEC, LPE, CPL, (LPE >= 16 ? 16 : 1)><<<grid, kThreads, 0, s>>>(a); break;
         default: sddmm_kernel<VEC, LPE, CPL, 32><<<grid, kThreads, 0, s>>>(a); break;
     }
     return cudaGetLastError();
@@ -472,17 +736,21 @@ template <int VEC>
 cudaError_t sddmm_dispatch(const SddmmArgs &a, int cph, cudaStream_t s) {
     const int64_t nch = ceil_div(a.H * a.Fh, VEC);
     if (nch <= 16) {
-        const int lpe = pow2ceil(nch < 4 ? 4 : nch);
+        // the lanes of one edge must cover a whole head: lpe >= cph
+        int lpe = pow2ceil(nch < 2 ? 2 : nch);
+        if (lpe < cph) lpe = cph;
+        if (lpe == 2) return sddmm_go_cph<VEC, 2, 1>(a, cph, 1, s);
         if (lpe == 4) return sddmm_go_cph<VEC, 4, 1>(a, cph, 1, s);
         if (lpe == 8) return sddmm_go_cph<VEC, 8, 1>(a, cph, 1, s);
-        return sddmm_go_cph<VEC, 16, 1>(a, cph, 1, s);
+        if (lpe == 16) return sddmm_go_cph<VEC, 16, 1>(a, cph, 1, s);
     }
-    const int64_t cpl_need = ceil_div(nch, 32);
-    switch (cpl_need) {
-        case 1: return sddmm_go_cph<VEC, 32, 1>(a, cph, 1, s);
-        case 2: return sddmm_go_cph<VEC, 32, 2>(a, cph, 1, s);
-        case 3: case 4: return sddmm_go_cph<VEC, 32, 4>(a, cph, 1, s);
-        default: return sddmm_go_cph<VEC, 32, 8>(a, cph, ceil_div(nch, 32 * 8), s);
+    constexpr int MAXCPL = VEC >= 8 ? 2 : 4;
+    const int64_t slabs = ceil_div(nch, 32 * MAXCPL);
+    const int64_t cpl = ceil_div(nch, 32 * slabs);
+    switch (cpl) {
+        case 1: return sddmm_go_cph<VEC, 32, 1>(a, cph, slabs, s);
+        case 2: return sddmm_go_cph<VEC, 32, 2>(a, cph, slabs, s);
+        default: return sddmm_go_cph<VEC, 32, MAXCPL>(a, cph, slabs, s);
     }
 }
 
@@ -490,22 +758,30 @@ cudaError_t sddmm_dispatch(const SddmmArgs &a, int cph, cudaStream_t s) {
 
 cudaError_t launch_spmm(const SpmmArgs &a, int mode, cudaStream_t s) {
     if (a.nrows == 0 || a.F == 0) return cudaSuccess;
-    bool v4 = (a.ldx % 4 == 0) && (a.ldo % 4 == 0) && aligned16(a.X) && aligned16(a.out) && a.F >= 4;
-    if (mode != kSpmmScaled) v4 = v4 && (a.Fh % 4 == 0);
-    return v4 ? spmm_dispatch<4>(a, mode, s) : spmm_dispatch<1>(a, mode, s);
+    const bool wmode = mode != kSpmmScaled;
+    if (wmode && a.H > kHMax) return cudaErrorNotSupported;   // api.cu rejects H > 16 first
+    auto ok_vec = [&](int v) {
+        return a.F >= v && a.ldx % v == 0 && a.ldo % 4 == 0 && aligned(a.X, 4 * v) && aligned(a.out, 16) &&
+               (!wmode || a.Fh % v == 0);
+    };
+    if (ok_vec(8)) return spmm_dispatch<8, 2>(a, mode, s);
+    if (ok_vec(4)) return spmm_dispatch<4, 4>(a, mode, s);
+    return spmm_dispatch<1, 4>(a, mode, s);
 }
 
 cudaError_t launch_sddmm(const SddmmArgs &a, cudaStream_t s) {
     if (a.nrows == 0 || a.H == 0) return cudaSuccess;
     auto is_pow2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
-    const bool v4 = (a.Fh % 4 == 0) && is_pow2(a.Fh / 4) && a.Fh / 4 <= 32 && (a.ldx % 4 == 0) &&
-                    (a.ldy % 4 == 0) && aligned16(a.X) && aligned16(a.Y);
-    if (v4) return sddmm_dispatch<4>(a, (int)(a.Fh / 4), s);
-    if (is_pow2(a.Fh) && a.Fh <= 32) return sddmm_dispatch<1>(a, (int)a.Fh, s);
-    dim3 grid = row_grid(a.nrows, 0, 1);
+    auto ok_vec = [&](int v) {
+        return a.Fh % v == 0 && is_pow2(a.Fh / v) && a.Fh / v <= 32 && a.ldx % v == 0 && a.ldy % v == 0 &&
+               aligned(a.X, 4 * v) && aligned(a.Y, 4 * v);
+    };
+    if (ok_vec(8)) return sddmm_dispatch<8>(a, (int)(a.Fh / 8), s);
+    if (ok_vec(4)) return sddmm_dispatch<4>(a, (int)(a.Fh / 4), s);
+    if (ok_vec(1)) return sddmm_dispatch<1>(a, (int)a.Fh, s);
     SddmmArgs g = a;
     g.n_heavy = 0;
-    sddmm_generic_kernel<<<grid, kThreads, 0, s>>>(g);
+    sddmm_generic_kernel<<<row_grid(a.nrows, 0, 1), kThreads, 0, s>>>(g);
     return cudaGetLastError();
 }
 
@@ -513,8 +789,8 @@ cudaError_t launch_softmax(const SoftmaxArgs &a, cudaStream_t s) {
     if (a.nrows == 0 || a.H == 0) return cudaSuccess;
     const bool contiguous = a.lde == a.H && a.ldo == a.H && a.H <= 32 && (32 % a.H) == 0;
     if (contiguous) {
-        dim3 grid = row_grid(a.nrows, a.n_heavy, 1);
-        if (a.H % 4 == 0 && aligned16(a.e) && aligned16(a.out)) softmax_kernel<4><<<grid, kThreads, 0, s>>>(a);
+        const dim3 grid = row_grid(a.nrows, a.n_heavy, 1);
+        if (a.H % 4 == 0 && aligned(a.e, 16) && aligned(a.out, 16)) softmax_kernel<4><<<grid, kThreads, 0, s>>>(a);
         else softmax_kernel<1><<<grid, kThreads, 0, s>>>(a);
         return cudaGetLastError();
     }

@@ -97,7 +97,8 @@ def _desc(t):
 def _stream(stream, device):
     import torch
     if stream is None:
-        stream = torch.cuda.current_stream(device)
+        # a host tensor is rejected by the library (GSP_ERR_ARG); pick any valid stream
+        stream = torch.cuda.current_stream(device if device.type == "cuda" else None)
     return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
 
 

@@ -1,0 +1,51 @@
+"""Per-op timing on a BASELINE config (CUDA events, L2 flushed between reps).
+usage: python tools/opbench.py [--config reddit] [--reps 10] [--ops gspmm_fwd,...] [--F 64]"""
+import argparse, json, os, sys, time
+import numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import datagen, paper_2402_03548_b200 as gsp
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="reddit")
+ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--ops", default="gspmm_fwd,gspmm_rev,gsddmm,edge_softmax,wfwd,wrev")
+ap.add_argument("--F", type=int, default=0)
+ap.add_argument("--ld", type=int, default=0)
+ap.add_argument("--tag", default=os.environ.get("GSP_TUNE_SPMM", ""))
+args = ap.parse_args()
+cfg = datagen.CONFIGS[args.config]
+V, src, dst = datagen.make_graph(cfg)
+G = gsp.Graph(V, src, dst, device=0)
+E = G.E
+F = args.F or cfg.F
+ld = args.ld or max(F, cfg.ld if not args.F else F)
+H = cfg.H or 8
+Fg = H * (cfg.Fh or 8)
+X = torch.from_numpy(datagen.uniform(1, V, F, ld=ld)).cuda()[:, :F]
+Z = torch.from_numpy(datagen.uniform(2, V, Fg)).cuda()
+out = torch.empty((V, F), device="cuda")
+outg = torch.empty((V, Fg), device="cuda")
+s = torch.empty((E, H), device="cuda")
+flush = torch.empty(512 << 18, device="cuda")
+ops = {
+    "gspmm_fwd": lambda: G.gspmm(X, 2, out=out),
+    "gspmm_rev": lambda: G.gspmm(X, 2, out=out, reverse=True),
+    "gsddmm": lambda: G.gsddmm(Z, Z, out=s),
+    "edge_softmax": lambda: G.edge_softmax(s, out=s),
+    "wfwd": lambda: G.gspmm_weighted(Z, s, out=outg),
+    "wrev": lambda: G.gspmm_weighted(Z, s, out=outg, reverse=True),
+}
+G.gsddmm(Z, Z, out=s); G.edge_softmax(s, out=s)
+res = {}
+for name in args.ops.split(","):
+    f = ops[name]
+    for _ in range(3):
+        f()
+    ts = []
+    for _ in range(args.reps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); f(); b.record(); torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    res[name] = round(float(np.median(ts)), 4)
+print(json.dumps({"tag": args.tag, "config": args.config, "F": F, "ms": res}))
