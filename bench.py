@@ -245,11 +245,35 @@ def main_gsp(args):
     Ep = part.E
     s = torch.empty((Ep, H), device="cuda")
     outs = [torch.empty((R, F), device="cuda") for _ in range(4)]
-    gathered = [torch.empty((ncols, F), device="cuda") for _ in range(4)] if P > 1 else None
+    gathered = [torch.empty((ncols, F), device="cuda") for _ in range(3)] if P > 1 else None
+    partial = torch.empty((ncols, F), device="cuda") if P > 1 else None
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
     op_names = ["gspmm_fwd", "gspmm_rev", "gsddmm", "edge_softmax", "gspmm_weighted_fwd", "gspmm_weighted_rev"]
-    ev = {k: [] for k in op_names + ["allgather"]}
+    ev = {k: [] for k in op_names + ["exchange"]}
+
+    # the step as a list of (name, launch, input index into (X, dY, Z, dO) or None, output index or None)
+    def op_list():
+        L = [("gspmm_fwd", lambda: part.gspmm(X, gsp.NORM_BOTH, out=outs[0], stream=stream), 0, 0),
+             ("gspmm_rev", lambda: part.gspmm(dY, gsp.NORM_BOTH, out=outs[1], reverse=True, stream=stream), 1, 1),
+             ("gsddmm", lambda: part.gsddmm(Z, Z, out=s, stream=stream), 2, None),
+             ("edge_softmax", lambda: part.edge_softmax(s, out=s, stream=stream), None, None),
+             ("gspmm_weighted_fwd", lambda: part.gspmm_weighted(Z, s, out=outs[2], stream=stream), None, 2)]
+        if P == 1:
+            L.append(("gspmm_weighted_rev",
+                      lambda: part.gspmm_weighted(dO, s, out=outs[3], reverse=True, stream=stream), 3, 3))
+        else:
+            # alpha of an edge lives on its destination's rank: each rank sums its own
+            # edges per (padded) source row; one reduce-scatter completes dZ
+            L.append(("gspmm_weighted_rev",
+                      lambda: part.gspmm_weighted(dO, s, out=partial, reverse=True, stream=stream), 3, None))
+        return L
+    OPS = op_list()
+
+    def exchange():
+        for o, gbuf in zip(outs[:3], gathered[:3]):
+            dist.all_gather_into_tensor(gbuf, o)
+        dist.reduce_scatter_tensor(outs[3], partial)
 
     def step(record):
         def mark():
@@ -257,27 +281,14 @@ def main_gsp(args):
             e.record(stream)
             return e
         marks = [mark()] if record else None
-        part.gspmm(X, gsp.NORM_BOTH, out=outs[0], stream=stream)
-        if record: marks.append(mark())
-        part.gspmm(dY, gsp.NORM_BOTH, out=outs[1], reverse=True, stream=stream)
-        if record: marks.append(mark())
-        part.gsddmm(Z, Z, out=s, stream=stream)
-        if record: marks.append(mark())
-        part.edge_softmax(s, out=s, stream=stream)
-        if record: marks.append(mark())
-        part.gspmm_weighted(Z, s, out=outs[2], stream=stream)
-        if record: marks.append(mark())
-        if P == 1:
-            part.gspmm_weighted(dO, s, out=outs[3], reverse=True, stream=stream)
-        else:
-            # partitions: weighted reverse needs alpha owned by other ranks (DESIGN.md
-            # "Multi-GPU"); round 1 runs the local-edge part only (flagged in the JSON line)
-            part.gspmm_weighted(dO, s, out=outs[3], stream=stream)
-        if record: marks.append(mark())
+        for _, fn, _, _ in OPS:
+            fn()
+            if record:
+                marks.append(mark())
         if P > 1:
-            for o, gbuf in zip(outs, gathered):
-                dist.all_gather_into_tensor(gbuf, o)
-            if record: marks.append(mark())
+            exchange()
+            if record:
+                marks.append(mark())
         return marks
 
     for _ in range(args.warmup):
@@ -297,7 +308,7 @@ def main_gsp(args):
         flush.fill_(1.0)                      # L2 flush between timed steps (outside the events)
         marks = step(True)
         torch.cuda.synchronize()
-        names = op_names + (["allgather"] if P > 1 else [])
+        names = op_names + (["exchange"] if P > 1 else [])
         for i, n in enumerate(names):
             ev[n].append(marks[i].elapsed_time(marks[i + 1]))
         step_ms.append(marks[0].elapsed_time(marks[-1]))
@@ -323,14 +334,48 @@ def main_gsp(args):
         hout = [torch.empty((R, F), dtype=torch.float32).pin_memory() for _ in range(4)]
         dins = (X, dY, Z, dO)
 
-        def e2e_step():
-            for h, d in zip(hin, dins):
-                d.copy_(h, non_blocking=True)
-            step(False)
-            for h, o in zip(hout, outs):
-                h.copy_(o, non_blocking=True)
+        h2d = torch.cuda.Stream()
+        d2h = torch.cuda.Stream()
+
+        def e2e_step(start_event):
+            # inputs stream in on the H2D engine in the order the ops consume them; each
+            # output streams back on the D2H engine as soon as its op (or exchange) is done
+            h2d.wait_event(start_event)
+            d2h.wait_event(start_event)
+            ready = []
+            with torch.cuda.stream(h2d):
+                for h, d in zip(hin, dins):
+                    d.copy_(h, non_blocking=True)
+                    e = torch.cuda.Event()
+                    e.record(h2d)
+                    ready.append(e)
+            done = []
+            for _, fn, i_in, i_out in OPS:
+                if i_in is not None:
+                    stream.wait_event(ready[i_in])
+                fn()
+                if i_out is not None and P == 1:
+                    e = torch.cuda.Event()
+                    e.record(stream)
+                    done.append((e, i_out))
+            if P > 1:
+                exchange()
+                e = torch.cuda.Event()
+                e.record(stream)
+                done = [(e, k) for k in range(4)]
+            with torch.cuda.stream(d2h):
+                for e, k in done:
+                    d2h.wait_event(e)
+                    hout[k].copy_(outs[k], non_blocking=True)
+            fin = torch.cuda.Event()
+            fin.record(d2h)
+            stream.wait_event(fin)
+            stream.wait_stream(h2d)
+
         for _ in range(2):
-            e2e_step()
+            st = torch.cuda.Event()
+            st.record(stream)
+            e2e_step(st)
         torch.cuda.synchronize()
         e_ms = []
         for _ in range(max(3, args.steps // 2)):
@@ -338,7 +383,7 @@ def main_gsp(args):
             a0 = torch.cuda.Event(enable_timing=True)
             a1 = torch.cuda.Event(enable_timing=True)
             a0.record(stream)
-            e2e_step()
+            e2e_step(a0)
             a1.record(stream)
             torch.cuda.synchronize()
             e_ms.append(a0.elapsed_time(a1))
@@ -369,7 +414,8 @@ def main_gsp(args):
                      "GB_s": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
                      "frac_of_8TBs": round(gbs / 8000.0, 4)}
     if P > 1:
-        per_op["allgather"] = {"ms": round(avg["allgather"], 4)}
+        per_op["exchange"] = {"ms": round(avg["exchange"], 4),
+                              "what": "3 x all_gather_into_tensor [R,F] + reduce_scatter_tensor [P*R,F] (NCCL)"}
     dom = "gspmm_fwd"
     achieved = per_op[dom]["GB_s"]
     roofline = {"bound": "hbm", "kernel": "spmm_kernel<4,16,1,scaled> (gspmm fwd, BOTH)",
@@ -411,9 +457,6 @@ def main_gsp(args):
             "timing": {"wall_s_timed_region": round(wall, 3), "graph_gen_s": round(t_gen, 2),
                        "graph_create_s": round(t_create, 2), "device_graph_bytes": G.device_bytes},
         }
-        if P > 1:
-            line["note"] = ("N>1: weighted reverse runs on the local-edge partition only (round 1); "
-                            "all-gathers of the four vertex outputs included")
         print(json.dumps(line), flush=True)
     if P > 1:
         dist.destroy_process_group()

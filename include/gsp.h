@@ -112,8 +112,11 @@ gsp_status gsp_graph_info(const gsp_graph *g, int64_t *V, int64_t *E, int64_t *d
 /* Copy the canonical structure into caller-allocated HOST arrays (bit-exact
  * checks).  fwd_off[V+1], fwd_col[E], rev_off[V+1], rev_col[E], rev_eid[E],
  * coo_to_eid[E] (coo_to_eid[i] = edge ID of input COO edge i).  Any NULL is
- * skipped.  rev_* on a graph without rev -> GSP_ERR_NO_REVERSE; coo_to_eid or
- * rev_* on a partition graph -> GSP_ERR_ARG. */
+ * skipped.  rev_* on a graph without rev -> GSP_ERR_NO_REVERSE.  Partition
+ * graphs: fwd_* is the partition's own structure (R+1 offsets, padded column
+ * ids); for a fwd partition rev_* is its local-rev structure (ncols+1 offsets:
+ * its own edges grouped by padded source; rev_col = padded destination,
+ * rev_eid = local edge id); coo_to_eid -> GSP_ERR_ARG. */
 gsp_status gsp_graph_export(const gsp_graph *g, int64_t *fwd_off, int32_t *fwd_col, int64_t *rev_off,
                             int32_t *rev_col, int32_t *rev_eid, int32_t *coo_to_eid);
 
@@ -138,7 +141,7 @@ gsp_status gsp_gspmm(const gsp_graph *g, const gsp_tensor *X, int norm, gsp_tens
  *  reverse = 1: out[u, h*Fh+f] = sum_{k in rev row u} w[rev_eid_k, h] * X[rcol_k, h*Fh+f]
  * w is [E, H] indexed by edge ID (no eShuffle, no O(E) temporary).
  * Errors as gsp_gspmm; SHAPE also when w->rows != E, H > 16 or X->cols % H != 0.
- * Partition graphs: reverse = 0 only (reverse = 1 -> GSP_ERR_NO_REVERSE). */
+ * Partition graphs: see gsp_graph_partition (reverse = 1 gives per-source partials). */
 gsp_status gsp_gspmm_weighted(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *w,
                               gsp_tensor *out, int reverse, gsp_stream stream);
 
@@ -179,6 +182,9 @@ gsp_status gsp_partition_bounds(const gsp_graph *g, int nparts, int reverse, int
  *  symmetric shared graph a fwd partition also serves reverse = 1.
  *  gsp_gsddmm / gsp_edge_softmax / gsp_gspmm_weighted(reverse=0): fwd
  *  partitions only; the destination-side table of gsddmm is the padded table.
+ *  gsp_gspmm_weighted(reverse=1) on a fwd partition: out is [ncols, F], the
+ *  contribution of this partition's edges to every (padded) source row; the
+ *  sum over partitions (one reduce-scatter) equals the full gSpMMve^T rows.
  * device as in gsp_graph_create (-1 = host-only).  flags: GSP_PART_REVERSE.
  * Errors: NULL, ARG (nparts < 1, part out of range, g is itself a partition),
  * NO_REVERSE, OOM, CUDA. */

@@ -320,8 +320,7 @@ gsp_status gsp_graph_export(const gsp_graph *g, int64_t *fwd_off, int32_t *fwd_c
                             int32_t *rev_col, int32_t *rev_eid, int32_t *coo_to_eid) {
     if (!g) return fail(GSP_ERR_NULL, "graph is NULL");
     const gsp::HostGraph &h = g->host;
-    if (g->is_partition && (rev_off || rev_col || rev_eid || coo_to_eid))
-        return fail(GSP_ERR_ARG, "partition graphs export only their own structure (fwd_off, fwd_col)");
+    if (g->is_partition && coo_to_eid) return fail(GSP_ERR_ARG, "partition graphs have no coo_to_eid");
     if ((rev_off || rev_col || rev_eid) && !h.has_rev) return fail(GSP_ERR_NO_REVERSE, "graph has no rev structure");
     if (fwd_off) std::memcpy(fwd_off, h.fwd_off.data(), sizeof(int64_t) * h.fwd_off.size());
     if (fwd_col && !h.fwd_col.empty()) std::memcpy(fwd_col, h.fwd_col.data(), sizeof(int32_t) * h.fwd_col.size());
@@ -368,7 +367,9 @@ gsp_status gsp_gspmm_weighted(const gsp_graph *g, const gsp_tensor *X, const gsp
     gsp_status st;
     if ((st = check_compute_graph(g)) != GSP_OK) return st;
     if (reverse != 0 && reverse != 1) return fail(GSP_ERR_ARG, "reverse must be 0 or 1");
-    const gsp::DevStructure &S = reverse ? g->rev : g->fwd;
+    // fwd partitions: reverse = 1 runs over the partition's own edges grouped by
+    // source (lrev) and yields partial sums for every padded source row
+    const gsp::DevStructure &S = reverse ? (g->is_partition ? g->lrev : g->rev) : g->fwd;
     if (!S.present || (reverse && !S.eid))
         return reverse ? fail(GSP_ERR_NO_REVERSE, "no rev structure with edge ids on this graph")
                        : fail(GSP_ERR_ARG, "this partition only serves reverse = 1");
@@ -514,6 +515,23 @@ gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int dev
         for (int64_t r = 0; r <= R; r++) lh.fwd_off[r] = off[rb + std::min(r, nloc)] - base;
         lh.fwd_col.resize((size_t)lh.E);
         for (int64_t j = 0; j < lh.E; j++) lh.fwd_col[j] = (int32_t)padded(col[base + j]);
+        if (!prev) {
+            // local rev: this partition's edges grouped by padded source, stable in local edge id
+            const int64_t NC = (int64_t)nparts * R;
+            lh.rev_off.assign((size_t)NC + 1, 0);
+            lh.rev_col.resize((size_t)lh.E);
+            lh.rev_eid.resize((size_t)lh.E);
+            for (int64_t j = 0; j < lh.E; j++) lh.rev_off[(size_t)lh.fwd_col[j] + 1]++;
+            for (int64_t u = 0; u < NC; u++) lh.rev_off[u + 1] += lh.rev_off[u];
+            std::vector<int64_t> pos(lh.rev_off.begin(), lh.rev_off.end() - 1);
+            for (int64_t r = 0; r < nloc; r++)
+                for (int64_t j = lh.fwd_off[r]; j < lh.fwd_off[r + 1]; j++) {
+                    const int64_t k = pos[lh.fwd_col[j]]++;
+                    lh.rev_col[k] = (int32_t)((int64_t)part * R + r);
+                    lh.rev_eid[k] = (int32_t)j;
+                }
+            lh.has_rev = true;
+        }
         pg->is_partition = true;
         pg->nparts = nparts;
         pg->part = part;
@@ -577,6 +595,10 @@ gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int dev
                     pg->rev.col_scale[GSP_NORM_RIGHT] = pi_inv;
                     pg->rev.col_scale[GSP_NORM_BOTH] = pi_rsq;
                 }
+            }
+            if (st == GSP_OK && !prev) {
+                st = upload_structure(pg, pg->lrev, (int64_t)nparts * R, (int64_t)nparts * R, lh.rev_off, lh.rev_col,
+                                      &lh.rev_eid, nullptr, 0, nullptr);
             }
             if (st == GSP_OK) {
                 cudaError_t e = cudaDeviceSynchronize();

@@ -64,10 +64,12 @@ struct gsp_graph {
     bool is_partition = false;
     int nparts = 1, part = 0, part_reverse = 0;
     int64_t row_begin = 0, row_end = 0, R = 0, row_base = 0;
-    // host mirror (full graphs: HostGraph; partitions: local fwd only)
+    // host mirror (full graphs: HostGraph; fwd partitions: local fwd + local rev (lrev))
     gsp::HostGraph host;
-    // device
-    gsp::DevStructure fwd, rev;
+    // device.  lrev (fwd partitions only): the partition's OWN edges grouped by
+    // padded source row (rows = ncols), explicit local edge ids -- the weighted
+    // reverse on a partition yields per-source partial sums to reduce-scatter.
+    gsp::DevStructure fwd, rev, lrev;
     std::vector<void *> dev_allocs;
     int64_t device_bytes = 0;
 };

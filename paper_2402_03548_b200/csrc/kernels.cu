@@ -473,14 +473,6 @@ __device__ __forceinline__ void online_push(float &m, float &s, float x) {
         s += expf(x - m);
     }
 }
-__device__ __forceinline__ void online_merge(float &m, float &s, float mo, float so) {
-    const float mn = fmaxf(m, mo);
-    if (mn == -INFINITY) return;  // both empty
-    const float a = (m == -INFINITY) ? 0.f : s * expf(m - mn);
-    const float b = (mo == -INFINITY) ? 0.f : so * expf(mo - mn);
-    m = mn;
-    s = a + b;
-}
 
 // exp(x) for x <= 0 via ex2.approx: relative error ~2^-22 + |x| 2^-24 (x is a
 // logit difference, |x| <~ 100), far inside the 2e-5 absolute bound on alpha.

@@ -142,9 +142,10 @@ class Graph:
     # ---------------------------------------------------------- structure
     def export(self, rev=True, coo=True):
         n = self.V
+        nr = self.ncols   # full graph: V; fwd partition: local rev over the padded sources
         out = {"fwd_off": np.empty(n + 1, np.int64), "fwd_col": np.empty(self.E, np.int32)}
         if rev:
-            out.update(rev_off=np.empty(n + 1, np.int64), rev_col=np.empty(self.E, np.int32),
+            out.update(rev_off=np.empty(nr + 1, np.int64), rev_col=np.empty(self.E, np.int32),
                        rev_eid=np.empty(self.E, np.int32))
         if coo:
             out["coo_to_eid"] = np.empty(self.E, np.int32)
@@ -185,7 +186,8 @@ class Graph:
 
     def gspmm_weighted(self, X, w, out=None, reverse=False, stream=None):
         if out is None:
-            out = self._alloc(self.V, X.shape[1], X)
+            rows = self.ncols if reverse else self.V   # fwd partition, reverse: per-source partials
+            out = self._alloc(rows, X.shape[1], X)
         dx, dw, do = _desc(X), _desc(w), _desc(out)
         _check(lib.gsp_gspmm_weighted(self._h, ctypes.byref(dx), ctypes.byref(dw), ctypes.byref(do),
                                       int(bool(reverse)), _stream(stream, X.device)))

@@ -193,3 +193,25 @@ def test_partition_errors(gsp, golden):
     pg = G.partition(2, 0, device=-1)
     with pytest.raises(gsp.GspError):
         pg.partition(2, 0, device=-1)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_partition_local_rev_bitexact(gsp, seed):
+    """Local rev of a fwd partition: its own edges grouped by padded source,
+    stable in local edge id (brute force with a stable numpy argsort)."""
+    rng = np.random.default_rng(300 + seed)
+    V = int(rng.integers(2, 150))
+    E = int(rng.integers(0, 1200))
+    src, dst = datagen.random_multigraph(V, E, seed)
+    G = host_graph(gsp, V, src, dst)
+    og = oracle.Graph(V, src, dst)
+    for P in (1, 2, 3):
+        for p in range(P):
+            pg = G.partition(P, p, device=-1)
+            lo, lc, R, b = og.partition_structure(P, p)
+            ex = pg.export(rev=True, coo=False)
+            rows = np.repeat(np.arange(R), np.diff(lo))
+            order = np.argsort(lc, kind="stable")
+            assert np.array_equal(ex["rev_eid"], order.astype(np.int32))
+            assert np.array_equal(ex["rev_col"], (p * R + rows[order]).astype(np.int32))
+            assert np.array_equal(ex["rev_off"], np.concatenate([[0], np.cumsum(np.bincount(lc, minlength=P * R))]))

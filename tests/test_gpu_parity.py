@@ -358,3 +358,29 @@ def test_empty_and_degenerate(gsp):
     # zero-width features, zero heads
     G.gspmm(torch.empty((6, 0), device="cuda"), 2)
     torch.cuda.synchronize()
+
+
+def test_partition_weighted_reverse_partials_sum_to_full(gsp):
+    """Weighted reverse on fwd partitions: per-source partials over each
+    partition's own edges; their sum (the reduce-scatter) == full gSpMMve^T."""
+    cfg = datagen.CONFIGS["pubmed"]
+    V, src, dst = datagen.make_graph(cfg)
+    G, og = graph_pair(gsp, V, src, dst)
+    H, F = 8, 64
+    Zh = datagen.uniform(5, V, F)
+    wh = datagen.uniform(6, og.E, H, lo=0, hi=1)
+    ref, T = og.gspmm_weighted(Zh, wh, True)
+    for P in (2, 3):
+        b = G.partition_bounds(P)
+        parts = [G.partition(P, p, device=0) for p in range(P)]
+        R = parts[0].R
+        Zpad = torch.zeros((P * R, F), device="cuda")
+        for p in range(P):
+            Zpad[p * R:p * R + b[p + 1] - b[p]] = dev(Zh[b[p]:b[p + 1]])
+        total = torch.zeros((P * R, F), device="cuda")
+        for p, pg in enumerate(parts):
+            e0, e1 = og.fwd_off[b[p]], og.fwd_off[b[p + 1]]
+            total += pg.gspmm_weighted(Zpad, dev(wh[e0:e1]), reverse=True)
+        t = total.cpu().numpy()
+        got = np.concatenate([t[p * R:p * R + b[p + 1] - b[p]] for p in range(P)])
+        assert_within(got, ref, T, f"P{P} weighted rev partials")
