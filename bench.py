@@ -418,7 +418,7 @@ def main_gsp(args):
                               "what": "3 x all_gather_into_tensor [R,F] + reduce_scatter_tensor [P*R,F] (NCCL)"}
     dom = "gspmm_fwd"
     achieved = per_op[dom]["GB_s"]
-    roofline = {"bound": "hbm", "kernel": "spmm_kernel<4,16,1,scaled> (gspmm fwd, BOTH)",
+    roofline = {"bound": "hbm", "kernel": "spmm_kernel<VEC=8,LPE=8,CPL=1,scaled> (gspmm fwd, BOTH norm)",
                 "achieved": achieved, "peak": peak, "peak_kind": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                 "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "alg_bytes_per_launch": bytes_of[dom],

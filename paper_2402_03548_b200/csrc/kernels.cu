@@ -84,6 +84,15 @@ __device__ __forceinline__ float ld_stream_f32(const float *p, uint64_t pol) {
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
     return v;
 }
+// one 32-byte edge-value row (H = 8) in a single 256-bit request: one L2 sector
+__device__ __forceinline__ void ld_stream_v8(float *d, const float *p, uint64_t pol) {
+    unsigned u0, u1, u2, u3, u4, u5, u6, u7;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=r"(u0), "=r"(u1), "=r"(u2), "=r"(u3), "=r"(u4), "=r"(u5), "=r"(u6), "=r"(u7)
+                 : "l"(p), "l"(pol));
+    d[0] = __uint_as_float(u0); d[1] = __uint_as_float(u1); d[2] = __uint_as_float(u2); d[3] = __uint_as_float(u3);
+    d[4] = __uint_as_float(u4); d[5] = __uint_as_float(u5); d[6] = __uint_as_float(u6); d[7] = __uint_as_float(u7);
+}
 __device__ __forceinline__ float4 ld_stream_f4(const float *p, uint64_t pol) {
     float4 v;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
@@ -195,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     }
     const uint32_t ldxb = (uint32_t)(a.ldx * 4);
     const int H = W ? (int)a.H : 0;
+    const bool w_al32 = W && (reinterpret_cast<uintptr_t>(a.w) & 31u) == 0;
     float *s_w = s_raw + warp * 32 * kHMax;
 
     // Summation: <= kFoldTiles*32/G terms per
@@ -227,11 +237,11 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
         if constexpr (W) {
             const float *wr = a.w + (int64_t)ev * a.ldw;
             float *dst = s_w + slot * H;
-            if (H == 8 && a.ldw == 8) {
-                float4 w0 = make_float4(0.f, 0.f, 0.f, 0.f), w1 = w0;
-                if (lane < n) { w0 = ld_stream_f4(wr, pol.stream); w1 = ld_stream_f4(wr + 4, pol.stream); }
-                reinterpret_cast<float4 *>(dst)[0] = w0;
-                reinterpret_cast<float4 *>(dst)[1] = w1;
+            if (H == 8 && a.ldw == 8 && w_al32) {
+                float wv8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                if (lane < n) ld_stream_v8(wv8, wr, pol.stream);
+                reinterpret_cast<float4 *>(dst)[0] = make_float4(wv8[0], wv8[1], wv8[2], wv8[3]);
+                reinterpret_cast<float4 *>(dst)[1] = make_float4(wv8[4], wv8[5], wv8[6], wv8[7]);
             } else {
                 for (int t = 0; t < H; t++) dst[t] = lane < n ? ld_stream_f32(wr + t, pol.stream) : 0.f;
             }
