@@ -79,11 +79,6 @@ __device__ __forceinline__ int ld_stream_i32(const int32_t *p, uint64_t pol) {
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
-__device__ __forceinline__ float ld_stream_f32(const float *p, uint64_t pol) {
-    float v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
-    return v;
-}
 // one 32-byte edge-value row (H = 8) in a single 256-bit request: one L2 sector
 __device__ __forceinline__ void ld_stream_v8(float *d, const float *p, uint64_t pol) {
     unsigned u0, u1, u2, u3, u4, u5, u6, u7;
@@ -93,12 +88,21 @@ __device__ __forceinline__ void ld_stream_v8(float *d, const float *p, uint64_t 
     d[0] = __uint_as_float(u0); d[1] = __uint_as_float(u1); d[2] = __uint_as_float(u2); d[3] = __uint_as_float(u3);
     d[4] = __uint_as_float(u4); d[5] = __uint_as_float(u5); d[6] = __uint_as_float(u6); d[7] = __uint_as_float(u7);
 }
-__device__ __forceinline__ float4 ld_stream_f4(const float *p, uint64_t pol) {
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
-    return v;
+
+// async global -> shared copies (LDGSTS): edge-value rows land in smem without
+// occupying registers; src_size 0 zero-fills (padding lanes)
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, int src_size) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gsrc), "r"(src_size) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void *sdst, const void *gsrc, int src_size) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(gsrc), "r"(src_size) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // plain (coherent) loads of data the caller may alias with the output (softmax in place)
 __device__ __forceinline__ float4 ld_f4(const float *p, uint64_t pol) {
     float4 v;
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     constexpr int SW = VEC * LPE * CPL;   // feature slab handled by this CTA
     constexpr bool W = MODE != kSpmmScaled;
     constexpr int RED = kWarps * SW;
-    constexpr int WS = W ? kWarps * 32 * kHMax : 0;
+    constexpr int WS = W ? 2 * kWarps * 32 * kHMax : 0;   // double-buffered weight rows
     __shared__ __align__(16) int2 s_pair[kWarps][32];
     __shared__ __align__(16) float s_raw[RED > WS ? RED : WS];   // weights during the walk, then heavy combine
 
@@ -204,8 +208,9 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     }
     const uint32_t ldxb = (uint32_t)(a.ldx * 4);
     const int H = W ? (int)a.H : 0;
-    const bool w_al32 = W && (reinterpret_cast<uintptr_t>(a.w) & 31u) == 0;
-    float *s_w = s_raw + warp * 32 * kHMax;
+    const bool w16 = W && (H % 4 == 0) && (a.ldw % 4 == 0) && (reinterpret_cast<uintptr_t>(a.w) & 15u) == 0;
+    // H = 8 rows (32 B, one sector): one 256-bit register load per lane, one tile ahead
+    const bool w8 = W && H == 8 && a.ldw == 8 && (reinterpret_cast<uintptr_t>(a.w) & 31u) == 0;
 
     // Summation: <= kFoldTiles*32/G terms per
     // lane summed plainly into `tile`, then folded into a Kahan-compensated
@@ -221,31 +226,78 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     }
     int ntile = 0;
 
-    for (int64_t base = b; base < e; base += 32) {
-        const int n = (int)(e - base < 32 ? e - base : 32);
-        // ---- stage this tile's (col, weight) pairs (and weight rows) in smem
-        int c = 0, ev = 0;
-        float wv = 0.f;
-        if (lane < n) {
-            c = ld_stream_i32(a.col + base + lane, pol.stream);
-            if constexpr (MODE == kSpmmScaled) wv = HAS_CS ? __ldg(a.col_scale + c) : 1.f;
-            else if constexpr (MODE == kSpmmWeightedFwd) ev = (int)(base + lane);
-            else ev = ld_stream_i32(a.eid + base + lane, pol.stream);
+    // Index pipeline: column ids (and rev edge ids) are
+    // loaded two tiles ahead, the dependent per-edge scale one tile ahead, and
+    // weight rows are copied global -> smem asynchronously one tile ahead
+    // (double buffer), so a tile's gathers never wait on its own index trips.
+    const int slot = (lane % G) * PER + lane / G;   // group-contiguous layout
+    auto load_idx = [&](int64_t tb, int &c, int &ev) {
+        c = 0;
+        ev = 0;
+        if (tb + lane < e) {
+            c = ld_stream_i32(a.col + tb + lane, pol.stream);
+            if constexpr (MODE == kSpmmWeightedFwd) ev = (int)(tb + lane);
+            else if constexpr (MODE == kSpmmWeightedRev) ev = ld_stream_i32(a.eid + tb + lane, pol.stream);
         }
-        const int slot = (lane % G) * PER + lane / G;   // group-contiguous layout
-        s_pair[warp][slot] = make_int2(c, __float_as_int(wv));
+    };
+    auto load_scale = [&](int64_t tb, int c) -> float {
+        if constexpr (MODE == kSpmmScaled) {
+            if (tb + lane < e) return HAS_CS ? __ldg(a.col_scale + c) : 1.f;
+        }
+        return 0.f;
+    };
+    auto load_w8 = [&](int64_t tb, int ev, float *d) {
         if constexpr (W) {
-            const float *wr = a.w + (int64_t)ev * a.ldw;
-            float *dst = s_w + slot * H;
-            if (H == 8 && a.ldw == 8 && w_al32) {
-                float wv8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                if (lane < n) ld_stream_v8(wv8, wr, pol.stream);
-                reinterpret_cast<float4 *>(dst)[0] = make_float4(wv8[0], wv8[1], wv8[2], wv8[3]);
-                reinterpret_cast<float4 *>(dst)[1] = make_float4(wv8[4], wv8[5], wv8[6], wv8[7]);
-            } else {
-                for (int t = 0; t < H; t++) dst[t] = lane < n ? ld_stream_f32(wr + t, pol.stream) : 0.f;
+            if (tb + lane < e) ld_stream_v8(d, a.w + (int64_t)ev * 8, pol.stream);
+            else {
+#pragma unroll
+                for (int t = 0; t < 8; t++) d[t] = 0.f;
             }
         }
+    };
+    auto issue_w = [&](int64_t tb, int ev, int buf) {
+        if constexpr (W) {
+            if (w8) return;
+            float *dst = s_raw + (buf * kWarps + warp) * 32 * kHMax + slot * H;
+            const bool valid = tb + lane < e;
+            const float *src = a.w + (int64_t)(valid ? ev : 0) * a.ldw;
+            if (w16) {
+                for (int t = 0; t < H; t += 4) cp_async16(dst + t, src + t, valid ? 16 : 0);
+            } else {
+                for (int t = 0; t < H; t++) cp_async4(dst + t, src + t, valid ? 4 : 0);
+            }
+            cp_async_commit();
+        }
+    };
+    int c1, e1, c2, e2;
+    load_idx(b, c1, e1);
+    load_idx(b + 32, c2, e2);
+    float wv1 = load_scale(b, c1);
+    float w8a[W ? 8 : 1];
+    if (w8) load_w8(b, e1, w8a);
+    else issue_w(b, e1, 0);
+    int buf = 0;
+
+    for (int64_t base = b; base < e; base += 32) {
+        const int n = (int)(e - base < 32 ? e - base : 32);
+        s_pair[warp][slot] = make_int2(c1, __float_as_int(wv1));
+        // ---- advance the pipeline before this tile's gathers
+        int c3, e3;
+        load_idx(base + 64, c3, e3);
+        const float wv2 = load_scale(base + 32, c2);
+        float w8b[W ? 8 : 1];
+        if constexpr (W) {
+            if (w8) {
+                float *dst = s_raw + (buf * kWarps + warp) * 32 * kHMax + slot * 8;
+                reinterpret_cast<float4 *>(dst)[0] = make_float4(w8a[0], w8a[1], w8a[2], w8a[3]);
+                reinterpret_cast<float4 *>(dst)[1] = make_float4(w8a[4], w8a[5], w8a[6], w8a[7]);
+                load_w8(base + 32, e2, w8b);
+            } else {
+                issue_w(base + 32, e2, buf ^ 1);
+                cp_async_wait<1>();   // this tile's weight rows have landed
+            }
+        }
+        const float *s_w = s_raw + (buf * kWarps + warp) * 32 * kHMax;
         __syncwarp();
         const int2 *gp = &s_pair[warp][g * PER];
         const float *gw = s_w + g * PER * H;
@@ -292,6 +344,12 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
             for (int i = 0; i < m; i += U) body(i, false, m);
         }
         __syncwarp();
+        c1 = c2; e1 = e2; c2 = c3; e2 = e3; wv1 = wv2;
+        buf ^= 1;
+        if constexpr (W) {
+#pragma unroll
+            for (int t = 0; t < 8; t++) w8a[t] = w8b[t];
+        }
         if (++ntile == kFoldTiles || base + 32 >= e) {
             ntile = 0;
 #pragma unroll
@@ -309,6 +367,7 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
                 }
         }
     }
+    if constexpr (W) cp_async_wait<0>();   // no copy may outlive the loop (smem is reused)
     // compensated totals, then the G edge groups of the warp (xor tree)
 #pragma unroll
     for (int q = 0; q < CPL; q++)
@@ -341,7 +400,8 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     }
     // heavy row: deterministic cross-warp combine in warp order
     float *red = s_raw;
-    __syncthreads();   // every warp is done with its s_w slice (aliased by red)
+    if constexpr (W) cp_async_wait<0>();
+    __syncthreads();   // every warp is done with its s_w slices (aliased by red)
     if (g == 0) {
 #pragma unroll
         for (int q = 0; q < CPL; q++)
@@ -400,11 +460,14 @@ __global__ void __launch_bounds__(kThreads, (VEC * CPL <= 8 ? 3 : 2)) sddmm_kern
     }
     const uint32_t ldyb = (uint32_t)(a.ldy * 4);
 
+    // column ids are loaded two tiles ahead of their gathers (index pipeline)
+    auto load_col = [&](int64_t tb) { return tb + lane < e ? ld_stream_i32(a.col + tb + lane, pol.stream) : 0; };
+    int c1 = load_col(b), c2 = load_col(b + 32);
     for (int64_t base = b; base < e; base += 32) {
         const int n = (int)(e - base < 32 ? e - base : 32);
-        int c = 0;
-        if (lane < n) c = ld_stream_i32(a.col + base + lane, pol.stream);
-        s_col[warp][(lane % G) * PER + lane / G] = c;
+        s_col[warp][(lane % G) * PER + lane / G] = c1;
+        c1 = c2;
+        c2 = load_col(base + 64);
         __syncwarp();
         const int *gp = &s_col[warp][g * PER];
         float *ob = a.out + (base + g) * a.ldo;   // group g's i-th edge is tile edge g + G*i
@@ -681,9 +744,9 @@ cudaError_t spmm_go(const SpmmArgs &a, int mode, int64_t slabs, cudaStream_t s) 
     if constexpr (VEC == 8 && LPE == 8 && CPL == 1) {
         switch (tune_spmm()) {
             case 0:   // measured best on B200 (Reddit-shaped F = 64, tools/opbench.py)
-                if (mode == kSpmmScaled) return spmm_go_v<VEC, LPE, CPL, 8, 3>(a, mode, slabs, s);
-                return spmm_go_v<VEC, LPE, CPL, 2, 4>(a, mode, slabs, s);
+                return spmm_go_v<VEC, LPE, CPL, 8, 2>(a, mode, slabs, s);
             case 5: return spmm_go_v<VEC, LPE, CPL>(a, mode, slabs, s);
+            case 6: return spmm_go_v<VEC, LPE, CPL, 4, 2>(a, mode, slabs, s);
             case 1: return spmm_go_v<VEC, LPE, CPL, 8, 2>(a, mode, slabs, s);
             case 2: return spmm_go_v<VEC, LPE, CPL, 4, 4>(a, mode, slabs, s);
             case 3: return spmm_go_v<VEC, LPE, CPL, 2, 4>(a, mode, slabs, s);
