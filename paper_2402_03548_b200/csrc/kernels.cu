@@ -422,12 +422,12 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
 
 // ================================================================ gSDDMMvv
 // out[j, h] = <X[row_base + v, head h], Y[col_j, head h]>; CPH = Fh / VEC lanes per head.
-template <int VEC, int LPE, int CPL, int CPH>
-__global__ void __launch_bounds__(kThreads, (VEC * CPL <= 8 ? 3 : 2)) sddmm_kernel(const SddmmArgs a) {
+template <int VEC, int LPE, int CPL, int CPH, int UOVR = 0, int MINB = 0>
+__global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 : 2))) sddmm_kernel(const SddmmArgs a) {
     constexpr int G = 32 / LPE;
     constexpr int PER = LPE;
     constexpr int UB = 32 / (VEC * CPL);
-    constexpr int U0 = UB < 2 ? 2 : (UB > 4 ? 4 : UB);
+    constexpr int U0 = UOVR ? UOVR : (UB < 2 ? 2 : (UB > 4 ? 4 : UB));
     constexpr int U = U0 > PER ? PER : U0;
     constexpr int SW = VEC * LPE * CPL;
     __shared__ __align__(16) int s_col[kWarps][32];
@@ -783,9 +783,28 @@ cudaError_t spmm_dispatch(const SpmmArgs &a, int mode, cudaStream_t s) {
     }
 }
 
+int tune_sddmm() {
+    static int v = [] {
+        const char *e = getenv("GSP_TUNE_SDDMM");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 template <int VEC, int LPE, int CPL>
 cudaError_t sddmm_go_cph(const SddmmArgs &a, int cph, int64_t slabs, cudaStream_t s) {
     const dim3 grid = row_grid(a.nrows, a.n_heavy, slabs);
+    if constexpr (VEC == 8 && LPE == 8 && CPL == 1) {
+        if (cph == 1) {
+            switch (tune_sddmm()) {
+                case 0:   // measured best on B200 (Reddit-shaped H = 8 x 8, tools/opbench.py)
+                case 2: sddmm_kernel<VEC, LPE, CPL, 1, 4, 4><<<grid, kThreads, 0, s>>>(a); return cudaGetLastError();
+                case 1: sddmm_kernel<VEC, LPE, CPL, 1, 8, 2><<<grid, kThreads, 0, s>>>(a); return cudaGetLastError();
+                case 3: sddmm_kernel<VEC, LPE, CPL, 1, 2, 4><<<grid, kThreads, 0, s>>>(a); return cudaGetLastError();
+                default: break;
+            }
+        }
+    }
     switch (cph) {
         case 1: sddmm_kernel<VEC, LPE, CPL, 1><<<grid, kThreads, 0, s>>>(a); break;
         case 2: sddmm_kernel<VEC, LPE, CPL, (LPE >= 2 ? 2 : 1)><<<grid, kThreads, 0, s>>>(a); break;
