@@ -161,6 +161,17 @@ gsp_status gsp_gsddmm(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor 
  * any other overlap is GSP_ERR_ALIAS.  Non-finite inputs propagate (IEEE). */
 gsp_status gsp_edge_softmax(const gsp_graph *g, const gsp_tensor *e, gsp_tensor *out, gsp_stream stream);
 
+/* Edge-softmax backward (GAT backward chain; the
+ * softmax Jacobian-vector product, "Backward Computation"):
+ *   dscore[j,h] = alpha[j,h] * (dalpha[j,h] - sum_{j' in fwd row of j} alpha[j',h] * dalpha[j',h])
+ * alpha = the forward edge_softmax output (state tensor), dalpha
+ * its gradient; all [E, H] by edge ID.  dscore == dalpha exactly is allowed
+ * (in place); any other overlap with dalpha, or any overlap with alpha, is
+ * GSP_ERR_ALIAS.  The rest of the GAT backward uses existing calls:
+ * dalpha = gsp_gsddmm(g, dOut, Z) and dZ = gsp_gspmm_weighted(reverse = 1). */
+gsp_status gsp_edge_softmax_backward(const gsp_graph *g, const gsp_tensor *alpha, const gsp_tensor *dalpha,
+                                     gsp_tensor *dscore, gsp_stream stream);
+
 /* -------------------------------------------------------------- multi-GPU */
 
 /* Edge-balanced contiguous row bounds:

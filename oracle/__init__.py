@@ -56,6 +56,8 @@ def _L():
         lib.oracle_gsddmm.restype = ci
         lib.oracle_edge_softmax.argtypes = [i64, p, p, i64, i64, p, p]
         lib.oracle_edge_softmax.restype = ci
+        lib.oracle_edge_softmax_backward.argtypes = [i64, p, p, p, i64, i64, p, p, p]
+        lib.oracle_edge_softmax_backward.restype = ci
         lib.oracle_partition_bounds.argtypes = [i64, p, i64, p]
         lib.oracle_partition_bounds.restype = ci
         lib.oracle_partition_structure.argtypes = [i64, p, p, i64, p, i64, p, p]
@@ -170,6 +172,21 @@ class Graph:
         rc = _L().oracle_edge_softmax(self.V, _ptr(self.fwd_off), _ptr(e), H, nsel, _ptr(sel), _ptr(out))
         assert rc == 0, rc
         return out
+
+    # --- C9 (NEXT-1)
+    def edge_softmax_backward(self, alpha, dalpha, rows=None):
+        alpha = _c(alpha, np.float32)
+        dalpha = _c(dalpha, np.float32)
+        H = alpha.shape[1]
+        assert alpha.shape == dalpha.shape and alpha.shape[0] == self.E
+        nsel, sel, _ = self._sel(rows)
+        m = self._nedges(rows)
+        out = np.empty((m, H), np.float64)
+        T = np.empty((m, H), np.float64)
+        rc = _L().oracle_edge_softmax_backward(self.V, _ptr(self.fwd_off), _ptr(alpha), _ptr(dalpha), H, nsel,
+                                               _ptr(sel), _ptr(out), _ptr(T))
+        assert rc == 0, rc
+        return out, T
 
     # --- C8
     def partition_bounds(self, nparts, reverse=False):

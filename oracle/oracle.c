@@ -245,6 +245,36 @@ int oracle_edge_softmax(int64_t V, const int64_t *fwd_off, const float *e, int64
     return 0;
 }
 
+/* ------------------------------------------------------------------ C9 --- */
+/* Edge-softmax backward (GAT backward chain; the chain
+ * rule through C7 -- P:1340-1341 "Backward Computation"):
+ *   ds[j,h] = alpha[j,h] * (dalpha[j,h] - sum_{j' in row v} alpha[j',h] * dalpha[j',h])
+ * T[j,h] = |alpha dalpha| + alpha * sum |alpha dalpha|.  Packed like C6/C7 with sel. */
+int oracle_edge_softmax_backward(int64_t V, const int64_t *fwd_off, const float *alpha, const float *dalpha,
+                                 int64_t H, int64_t nsel, const int64_t *sel, double *out, double *T) {
+    int64_t n = sel ? nsel : V, o = 0;
+    for (int64_t r = 0; r < n; r++) {
+        int64_t v = sel ? sel[r] : r;
+        if (v < 0 || v >= V) return -1;
+        int64_t b = fwd_off[v], en = fwd_off[v + 1];
+        for (int64_t h = 0; h < H; h++) {
+            double d = 0.0, dabs = 0.0;
+            for (int64_t j = b; j < en; j++) {
+                double t = (double)alpha[j * H + h] * (double)dalpha[j * H + h];
+                d += t;
+                dabs += fabs(t);
+            }
+            for (int64_t j = b; j < en; j++) {
+                double a = (double)alpha[j * H + h], g = (double)dalpha[j * H + h];
+                out[(o + (j - b)) * H + h] = a * (g - d);
+                if (T) T[(o + (j - b)) * H + h] = fabs(a * g) + fabs(a) * dabs;
+            }
+        }
+        o += en - b;
+    }
+    return 0;
+}
+
 /* ------------------------------------------------------------------ C8 --- */
 /* Edge-balanced contiguous row partition (BJ north_star
  * "destination-row partitioner"):  b_0 = 0, b_P = V,

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -218,6 +219,14 @@ static gsp_status upload_full(gsp_graph *g) {
     if (!dg.ok) return fail(GSP_ERR_ARG, "cannot select device " + std::to_string(g->device));
     if (const char *pm = getenv("GSP_L2_PERSIST_MB")) {   // experiment knob
         cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atol(pm) << 20);
+        cudaGetLastError();
+    }
+    if (const char *fg = getenv("GSP_L2_FETCH")) {        // experiment knob: L2 fetch granularity (bytes)
+        size_t before = 0, after = 0;
+        cudaDeviceGetLimit(&before, cudaLimitMaxL2FetchGranularity);
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atol(fg));
+        cudaDeviceGetLimit(&after, cudaLimitMaxL2FetchGranularity);
+        fprintf(stderr, "gsp: L2 fetch granularity %zu -> %zu\n", before, after);
         cudaGetLastError();
     }
     gsp_status st;
@@ -450,6 +459,32 @@ gsp_status gsp_edge_softmax(const gsp_graph *g, const gsp_tensor *e_in, gsp_tens
     a.H = e_in->cols;
     cudaError_t err = gsp::launch_softmax(a, (cudaStream_t)stream);
     if (err != cudaSuccess) return cuda_fail(err, "edge_softmax launch");
+    return GSP_OK;
+}
+
+gsp_status gsp_edge_softmax_backward(const gsp_graph *g, const gsp_tensor *alpha, const gsp_tensor *dalpha,
+                                     gsp_tensor *dscore, gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    const gsp::DevStructure &S = g->fwd;
+    if (!S.present) return fail(GSP_ERR_ARG, "edge_softmax_backward needs the fwd structure");
+    if (!alpha || !dalpha || !dscore) return fail(GSP_ERR_NULL, "alpha/dalpha/dscore is NULL");
+    if ((st = check_tensor(g, alpha, "alpha", g->E, -1)) != GSP_OK) return st;
+    if ((st = check_tensor(g, dalpha, "dalpha", g->E, alpha->cols)) != GSP_OK) return st;
+    if ((st = check_tensor(g, dscore, "dscore", g->E, alpha->cols)) != GSP_OK) return st;
+    if (overlaps(alpha, dscore)) return fail(GSP_ERR_ALIAS, "dscore overlaps alpha");
+    const bool same = dalpha->data == dscore->data && dalpha->ld == dscore->ld;
+    if (!same && overlaps(dalpha, dscore)) return fail(GSP_ERR_ALIAS, "dscore partially overlaps dalpha");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    gsp::SoftmaxBwdArgs a{};
+    a.off = S.off; a.order = S.order; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.alpha = static_cast<const float *>(alpha->data); a.lda = alpha->ld;
+    a.dalpha = static_cast<const float *>(dalpha->data); a.ldd = dalpha->ld;
+    a.out = static_cast<float *>(dscore->data); a.ldo = dscore->ld;
+    a.H = alpha->cols;
+    cudaError_t e = gsp::launch_softmax_bwd(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "edge_softmax_backward launch");
     return GSP_OK;
 }
 

@@ -694,6 +694,63 @@ __global__ void __launch_bounds__(kThreads) softmax_generic_kernel(const Softmax
     }
 }
 
+// ==================================================== edge softmax backward
+// ds[j,h] = alpha[j,h] * (dalpha[j,h] - <alpha[row,h], dalpha[row,h]>)   (NEXT-1)
+// Fast path: contiguous [E, H], H % 4 == 0, H | 32 (lane owns heads (4 lane + t) mod H).
+__global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const SoftmaxBwdArgs a) {
+    __shared__ float sm_d[kWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int H = (int)a.H, HPL = H / 4;
+    int64_t row, b, e;
+    bool heavy;
+    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    const Pol pol = make_pol();
+    const int64_t lo = b * H, hi = e * H;
+    float d[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int64_t i = lo + (int64_t)lane * 4; i < hi; i += 128) {
+        const float4 x = ld_f4(a.alpha + i, pol.keep), y = ld_f4(a.dalpha + i, pol.keep);
+        d[0] = fmaf(x.x, y.x, d[0]); d[1] = fmaf(x.y, y.y, d[1]);
+        d[2] = fmaf(x.z, y.z, d[2]); d[3] = fmaf(x.w, y.w, d[3]);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; t++)
+        for (int o = HPL; o < 32; o <<= 1) d[t] += __shfl_xor_sync(kFull, d[t], o);
+    if (heavy) {
+        if (lane < HPL)
+#pragma unroll
+            for (int t = 0; t < 4; t++) sm_d[warp][lane * 4 + t] = d[t];
+        __syncthreads();
+        const int hl = lane % HPL;
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            float acc = 0.f;
+            for (int w = 0; w < kWarps; w++) acc += sm_d[w][hl * 4 + t];
+            d[t] = acc;
+        }
+    }
+    for (int64_t i = lo + (int64_t)lane * 4; i < hi; i += 128) {
+        const float4 x = ld_f4(a.alpha + i, pol.stream), y = ld_f4(a.dalpha + i, pol.stream);
+        st_stream_f4(a.out + i, make_float4(x.x * (y.x - d[0]), x.y * (y.y - d[1]), x.z * (y.z - d[2]),
+                                            x.w * (y.w - d[3])), pol.stream);
+    }
+}
+
+// generic (any H, any ld): one warp per row, lanes over heads
+__global__ void __launch_bounds__(kThreads) softmax_bwd_generic_kernel(const SoftmaxBwdArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t row, b, e;
+    bool heavy;
+    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    for (int64_t h = lane; h < a.H; h += 32) {
+        float d = 0.f;
+        for (int64_t j = b; j < e; j++) d = fmaf(a.alpha[j * a.lda + h], a.dalpha[j * a.ldd + h], d);
+        for (int64_t j = b; j < e; j++) {
+            const float x = a.alpha[j * a.lda + h], y = a.dalpha[j * a.ldd + h];
+            a.out[j * a.ldo + h] = x * (y - d);
+        }
+    }
+}
+
 __global__ void degree_scales_kernel(const int64_t *deg, int64_t n, float *inv, float *rsq) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double d = deg[i] < 1 ? 1.0 : (double)deg[i];   // clamp d^ = max(d, 1)
@@ -881,6 +938,20 @@ cudaError_t launch_softmax(const SoftmaxArgs &a, cudaStream_t s) {
     SoftmaxArgs g = a;
     g.n_heavy = 0;
     softmax_generic_kernel<<<row_grid(a.nrows, 0, 1), kThreads, 0, s>>>(g);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_softmax_bwd(const SoftmaxBwdArgs &a, cudaStream_t s) {
+    if (a.nrows == 0 || a.H == 0) return cudaSuccess;
+    const bool fast = a.lda == a.H && a.ldd == a.H && a.ldo == a.H && a.H % 4 == 0 && a.H <= 32 && (32 % a.H) == 0 &&
+                      aligned(a.alpha, 16) && aligned(a.dalpha, 16) && aligned(a.out, 16);
+    if (fast) {
+        softmax_bwd_kernel<<<row_grid(a.nrows, a.n_heavy, 1), kThreads, 0, s>>>(a);
+    } else {
+        SoftmaxBwdArgs g = a;
+        g.n_heavy = 0;
+        softmax_bwd_generic_kernel<<<row_grid(a.nrows, 0, 1), kThreads, 0, s>>>(g);
+    }
     return cudaGetLastError();
 }
 

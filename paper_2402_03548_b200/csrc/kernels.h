@@ -57,6 +57,21 @@ struct SoftmaxArgs {
 };
 cudaError_t launch_softmax(const SoftmaxArgs &a, cudaStream_t s);
 
+// Edge-softmax backward: ds = alpha * (dalpha - sum_row alpha*dalpha).
+struct SoftmaxBwdArgs {
+    const int64_t *off;
+    const int32_t *order;
+    int64_t nrows, n_heavy;
+    const float *alpha;
+    int64_t lda;
+    const float *dalpha;
+    int64_t ldd;
+    float *out;
+    int64_t ldo;
+    int64_t H;
+};
+cudaError_t launch_softmax_bwd(const SoftmaxBwdArgs &a, cudaStream_t s);
+
 // fp32 degree scales from (clamped) integer degrees: inv = 1/d^, rsq = d^^-1/2
 // computed in fp64 then rounded once.
 cudaError_t launch_degree_scales(const int64_t *deg, int64_t n, float *inv, float *rsq, cudaStream_t s);

@@ -26,7 +26,8 @@ STATUS = {0: "GSP_OK", 1: "GSP_ERR_NULL", 2: "GSP_ERR_ARG", 3: "GSP_ERR_VERTEX_R
 
 # the exported C symbols (include/gsp.h), checked by tests/test_abi.py
 SYMBOLS = ["gsp_graph_create", "gsp_graph_destroy", "gsp_graph_info", "gsp_graph_export", "gsp_gspmm",
-           "gsp_gspmm_weighted", "gsp_gsddmm", "gsp_edge_softmax", "gsp_partition_bounds", "gsp_graph_partition",
+           "gsp_gspmm_weighted", "gsp_gsddmm", "gsp_edge_softmax", "gsp_edge_softmax_backward",
+           "gsp_partition_bounds", "gsp_graph_partition",
            "gsp_partition_info", "gsp_status_string", "gsp_last_error_detail", "gsp_version"]
 
 
@@ -59,6 +60,7 @@ def _load():
         "gsp_gspmm_weighted": ([p, T, T, T, ci, p], ci),
         "gsp_gsddmm": ([p, T, T, T, p], ci),
         "gsp_edge_softmax": ([p, T, T, p], ci),
+        "gsp_edge_softmax_backward": ([p, T, T, T, p], ci),
         "gsp_partition_bounds": ([p, ci, ci, p], ci),
         "gsp_graph_partition": ([p, ci, ci, ci, u32, P(p)], ci),
         "gsp_partition_info": ([p, P(ci), P(ci), P(i64), P(i64), P(i64), P(i64), P(ci)], ci),
@@ -207,6 +209,18 @@ class Graph:
         de, do = _desc(e), _desc(out)
         _check(lib.gsp_edge_softmax(self._h, ctypes.byref(de), ctypes.byref(do), _stream(stream, e.device)))
         return out
+
+
+def _edge_softmax_backward(self, alpha, dalpha, out=None, stream=None):
+    if out is None:
+        out = self._alloc(self.E, alpha.shape[1], alpha)
+    da, dd, do = _desc(alpha), _desc(dalpha), _desc(out)
+    _check(lib.gsp_edge_softmax_backward(self._h, ctypes.byref(da), ctypes.byref(dd), ctypes.byref(do),
+                                         _stream(stream, alpha.device)))
+    return out
+
+
+Graph.edge_softmax_backward = _edge_softmax_backward
 
 
 def version():

@@ -384,3 +384,25 @@ def test_partition_weighted_reverse_partials_sum_to_full(gsp):
         t = total.cpu().numpy()
         got = np.concatenate([t[p * R:p * R + b[p + 1] - b[p]] for p in range(P)])
         assert_within(got, ref, T, f"P{P} weighted rev partials")
+
+
+# ---------------------------------------------------- NEXT-1: softmax backward
+@pytest.mark.parametrize("H,ld", [(1, 1), (4, 4), (8, 8), (8, 12), (32, 32), (3, 3)])
+def test_softmax_backward_random(gsp, H, ld):
+    for seed in range(2):
+        rng = np.random.default_rng(seed + 11 * H)
+        V = int(rng.integers(1, 2500))
+        E = int(rng.integers(0, 40000))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed == 0
+                    else datagen.skewed_multigraph(V, E, seed, alpha=1.7))
+        G, og = graph_pair(gsp, V, src, dst)
+        if E == 0:
+            continue
+        ah = og.edge_softmax(datagen.uniform(seed, E, H, lo=-6, hi=6)).astype(np.float32)
+        gh = datagen.uniform(seed + 1, E, H)
+        ref, T = og.edge_softmax_backward(ah, gh)
+        out = G.edge_softmax_backward(padded(ah, ld), padded(gh, ld))
+        assert_within(out.cpu().numpy(), ref, T, f"H{H} ld{ld}")
+        g = dev(gh)
+        G.edge_softmax_backward(dev(ah), g, out=g)                 # in place on dalpha
+        assert_within(g.cpu().numpy(), ref, T, f"H{H} in place")

@@ -433,3 +433,50 @@ def test_partition_structure_concatenates_to_full(seed):
                 for j in range(lo[r], lo[r + 1]):
                     loc[r] += Xpad[lc[j]]
             assert np.allclose(loc[:b[p + 1] - b[p]], full[b[p]:b[p + 1]], atol=1e-12)
+
+
+# ------------------------------------------------- C9 softmax backward (NEXT-1)
+@pytest.mark.parametrize("seed", range(20))
+def test_softmax_backward_directional_derivative(seed):
+    """<dalpha, (softmax(e + eps d) - softmax(e - eps d)) / 2 eps> == <ds, d>: the
+    backward is pinned to the (already pinned) forward by central differences."""
+    V, src, dst = rand_graph(8000 + seed, Vmax=40, Emax=200)
+    G = oracle.Graph(V, src, dst)
+    if G.E == 0:
+        return
+    H = 1 + seed % 3
+    e = datagen.uniform(seed, G.E, H, lo=-3, hi=3).astype(np.float64)
+    g = datagen.uniform(seed + 1, G.E, H)
+    d = datagen.uniform(seed + 2, G.E, H).astype(np.float64)
+    a = G.edge_softmax(e.astype(np.float32))
+    ds, _ = G.edge_softmax_backward(a.astype(np.float32), g)
+    # forward on fp64-exact shifts: perturb in fp32-representable steps, use the fp64 oracle
+    eps = 2.0 ** -12
+    ap = G.edge_softmax((e + eps * d).astype(np.float32))
+    am = G.edge_softmax((e - eps * d).astype(np.float32))
+    dp = (e + eps * d).astype(np.float32).astype(np.float64) - (e - eps * d).astype(np.float32).astype(np.float64)
+    lhs = np.sum(g.astype(np.float64) * (ap - am))
+    rhs = np.sum(ds * dp)
+    assert abs(lhs - rhs) <= 1e-5 * (1 + abs(rhs)), (lhs, rhs)
+
+
+def test_softmax_backward_closed_forms(golden):
+    g4 = golden("d4.json")
+    G = oracle.Graph(g4["V"], g4["src"], g4["dst"])
+    a = G.edge_softmax(datagen.uniform(3, G.E, 2))
+    # uniform upstream gradient per row -> zero (softmax is shift invariant)
+    ds, _ = G.edge_softmax_backward(a.astype(np.float32), np.full((G.E, 2), 0.75, np.float32))
+    assert np.allclose(ds, 0, atol=1e-7)
+    # single-edge rows (D4 rows 0 and 1) -> zero; every row sums to zero
+    gr = datagen.uniform(4, G.E, 2)
+    ds, _ = G.edge_softmax_backward(a.astype(np.float32), gr)
+    assert np.allclose(ds[:2], 0, atol=1e-12)
+    assert np.allclose(ds[2:7].sum(0), 0, atol=1e-6)
+    # two-edge row closed form: ds1 = p (1 - p) (g1 - g2)
+    G2 = oracle.Graph(2, [0, 1], [0, 0])
+    al = np.array([[0.3], [0.7]], np.float32)
+    gg = np.array([[2.0], [-1.0]], np.float32)
+    ds, _ = G2.edge_softmax_backward(al, gg)
+    p = np.float64(np.float32(0.3)); q = np.float64(np.float32(0.7))
+    assert ds[0, 0] == pytest.approx(p * (2.0 - (p * 2.0 - q)), abs=1e-15)
+    assert ds[0, 0] == pytest.approx(p * q * 3.0, rel=1e-6)
