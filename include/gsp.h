@@ -172,6 +172,19 @@ gsp_status gsp_edge_softmax(const gsp_graph *g, const gsp_tensor *e, gsp_tensor 
 gsp_status gsp_edge_softmax_backward(const gsp_graph *g, const gsp_tensor *alpha, const gsp_tensor *dalpha,
                                      gsp_tensor *dscore, gsp_stream stream);
 
+/* Fused GAT forward (the fusion P:197 / P:1472-1484 asks
+ * for, that still materialises the state tensor alpha):
+ *   alpha = edge_softmax(gsddmm(X, Y))   [E, H] by edge ID   (as gsp_gsddmm + gsp_edge_softmax)
+ *   out   = gspmm_weighted(Vt, alpha)    [nrows, Vt->cols]   (as gsp_gspmm_weighted, reverse = 0)
+ * computed in one pass per destination row (online softmax) when the head
+ * width is 8 (X->cols = Vt->cols = 8 H, H in {2,4,8,16}, alpha->ld == H,
+ * 32-byte aligned tables), else by the three kernels in sequence.  Vt == Y
+ * (AGNN-style) is allowed and gathered once.  1 <= H <= 16.  Errors: NULL,
+ * ARG, SHAPE, ALIAS (out or alpha overlapping an input, out overlapping
+ * alpha), CUDA. */
+gsp_status gsp_gat_forward(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *Y, const gsp_tensor *Vt,
+                           gsp_tensor *alpha, gsp_tensor *out, gsp_stream stream);
+
 /* -------------------------------------------------------------- multi-GPU */
 
 /* Edge-balanced contiguous row bounds:

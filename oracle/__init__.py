@@ -58,6 +58,8 @@ def _L():
         lib.oracle_edge_softmax.restype = ci
         lib.oracle_edge_softmax_backward.argtypes = [i64, p, p, p, i64, i64, p, p, p]
         lib.oracle_edge_softmax_backward.restype = ci
+        lib.oracle_gat_forward.argtypes = [i64, p, p, p, i64, p, i64, i64, p, i64, i64, i64, p, p, p, p]
+        lib.oracle_gat_forward.restype = ci
         lib.oracle_partition_bounds.argtypes = [i64, p, i64, p]
         lib.oracle_partition_bounds.restype = ci
         lib.oracle_partition_structure.argtypes = [i64, p, p, i64, p, i64, p, p]
@@ -187,6 +189,24 @@ class Graph:
                                                _ptr(sel), _ptr(out), _ptr(T))
         assert rc == 0, rc
         return out, T
+
+    # --- C10 (NEXT-2)
+    def gat_forward(self, X, Y, Vt, H):
+        """(alpha [E,H], out [V,Fv], T_out) in fp64: softmax(gsddmm(X,Y)) then weighted sum of Vt."""
+        X = _c(X, np.float32)
+        Y = _c(Y, np.float32)
+        Vt = _c(Vt, np.float32)
+        F, Fv = X.shape[1], Vt.shape[1]
+        alpha = np.empty((self.E, H), np.float64)
+        out = np.empty((self.V, Fv), np.float64)
+        T = np.empty((self.V, Fv), np.float64)
+        maxdeg = int(np.max(np.diff(self.fwd_off))) if self.V else 0
+        scratch = np.empty(max(maxdeg, 1), np.float64)
+        rc = _L().oracle_gat_forward(self.V, _ptr(self.fwd_off), _ptr(self.fwd_col), _ptr(X), X.shape[1], _ptr(Y),
+                                     Y.shape[1], F, _ptr(Vt), Vt.shape[1], Fv, H, _ptr(alpha), _ptr(out), _ptr(T),
+                                     _ptr(scratch))
+        assert rc == 0, rc
+        return alpha, out, T
 
     # --- C8
     def partition_bounds(self, nparts, reverse=False):

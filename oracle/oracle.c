@@ -275,6 +275,49 @@ int oracle_edge_softmax_backward(int64_t V, const int64_t *fwd_off, const float 
     return 0;
 }
 
+/* ----------------------------------------------------------------- C10 --- */
+/* GAT forward as one definition (P:1329 Class A):
+ * for each destination row v and head h, over the slots j of row v (u = col_j):
+ *   s_j   = sum_{f < Fh} X[v, h*Fh+f] * Y[u, h*Fh+f]                      (C6)
+ *   a_j   = exp(s_j - max s) / sum exp(s - max s)                          (C7)
+ *   out[v, h*Fv+f] = sum_j a_j * Vt[u, h*Fv+f]                             (C5)
+ * all in fp64 (no fp32 hand-off between the steps).  alpha is written by
+ * edge ID; T_out = sum_j a_j |Vt|.  The scratch s (size = max degree) is the
+ * caller's. */
+int oracle_gat_forward(int64_t V, const int64_t *fwd_off, const int32_t *fwd_col, const float *X, int64_t ldx,
+                       const float *Y, int64_t ldy, int64_t F, const float *Vt, int64_t ldv, int64_t Fv, int64_t H,
+                       double *alpha, double *out, double *Tout, double *scratch) {
+    if (H <= 0 || F % H != 0 || Fv % H != 0) return -2;
+    int64_t Fh = F / H, Fvh = Fv / H;
+    for (int64_t v = 0; v < V; v++) {
+        int64_t b = fwd_off[v], e = fwd_off[v + 1];
+        for (int64_t h = 0; h < H; h++) {
+            double m = -INFINITY;
+            for (int64_t j = b; j < e; j++) {
+                int64_t u = fwd_col[j];
+                double sc = 0.0;
+                for (int64_t f = 0; f < Fh; f++) sc += (double)X[v * ldx + h * Fh + f] * (double)Y[u * ldy + h * Fh + f];
+                scratch[j - b] = sc;
+                if (sc > m) m = sc;
+            }
+            double S = 0.0;
+            for (int64_t j = b; j < e; j++) S += exp(scratch[j - b] - m);
+            for (int64_t j = b; j < e; j++) alpha[j * H + h] = exp(scratch[j - b] - m) / S;
+            for (int64_t f = 0; f < Fvh; f++) {
+                double acc = 0.0, tacc = 0.0;
+                for (int64_t j = b; j < e; j++) {
+                    double t = alpha[j * H + h] * (double)Vt[(int64_t)fwd_col[j] * ldv + h * Fvh + f];
+                    acc += t;
+                    tacc += fabs(t);
+                }
+                out[v * Fv + h * Fvh + f] = acc;
+                if (Tout) Tout[v * Fv + h * Fvh + f] = tacc;
+            }
+        }
+    }
+    return 0;
+}
+
 /* ------------------------------------------------------------------ C8 --- */
 /* Edge-balanced contiguous row partition (BJ north_star
  * "destination-row partitioner"):  b_0 = 0, b_P = V,

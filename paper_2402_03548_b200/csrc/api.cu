@@ -488,6 +488,68 @@ gsp_status gsp_edge_softmax_backward(const gsp_graph *g, const gsp_tensor *alpha
     return GSP_OK;
 }
 
+gsp_status gsp_gat_forward(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *Y, const gsp_tensor *Vt,
+                           gsp_tensor *alpha, gsp_tensor *out, gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    const gsp::DevStructure &S = g->fwd;
+    if (!S.present) return fail(GSP_ERR_ARG, "gat_forward needs the fwd structure (not a reverse partition)");
+    if (!X || !Y || !Vt || !alpha || !out) return fail(GSP_ERR_NULL, "X/Y/Vt/alpha/out is NULL");
+    if ((st = check_tensor(g, alpha, "alpha", g->E, -1)) != GSP_OK) return st;
+    const int64_t H = alpha->cols;
+    if (H < 1 || H > 16) return fail(GSP_ERR_SHAPE, "alpha must have 1 <= H <= 16 columns (heads)");
+    if ((st = check_tensor(g, X, "X", S.ncols, -1)) != GSP_OK) return st;
+    if ((st = check_tensor(g, Y, "Y", S.ncols, X->cols)) != GSP_OK) return st;
+    if ((st = check_tensor(g, Vt, "Vt", S.ncols, -1)) != GSP_OK) return st;
+    if ((st = check_tensor(g, out, "out", S.nrows, Vt->cols)) != GSP_OK) return st;
+    if (X->cols % H != 0 || Vt->cols % H != 0) return fail(GSP_ERR_SHAPE, "X.cols and Vt.cols must be multiples of H");
+    if (overlaps(out, X) || overlaps(out, Y) || overlaps(out, Vt) || overlaps(out, alpha))
+        return fail(GSP_ERR_ALIAS, "out overlaps an input or alpha");
+    if (overlaps(alpha, X) || overlaps(alpha, Y) || overlaps(alpha, Vt))
+        return fail(GSP_ERR_ALIAS, "alpha overlaps X, Y or Vt");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    cudaStream_t cs = (cudaStream_t)stream;
+    gsp::GatArgs ga{};
+    ga.off = S.off; ga.col = S.col; ga.order = S.order; ga.nrows = S.nrows; ga.n_heavy = S.n_heavy;
+    ga.row_base = g->row_base;
+    ga.X = static_cast<const float *>(X->data); ga.ldx = X->ld;
+    ga.Y = static_cast<const float *>(Y->data); ga.ldy = Y->ld;
+    ga.Vt = static_cast<const float *>(Vt->data); ga.ldv = Vt->ld;
+    ga.alpha = static_cast<float *>(alpha->data);
+    ga.out = static_cast<float *>(out->data); ga.ldo = out->ld;
+    ga.H = H;
+    const bool fused = X->cols == 8 * H && Vt->cols == 8 * H && alpha->ld == H && gsp::gat_fused_supported(ga);
+    cudaError_t e;
+    if (fused) {
+        e = gsp::launch_gat_fused(ga, cs);
+    } else {
+        // any other shape: the three kernels in sequence (same results within the bound)
+        gsp::SddmmArgs sa{};
+        sa.off = S.off; sa.col = S.col; sa.order = S.order; sa.nrows = S.nrows; sa.n_heavy = S.n_heavy;
+        sa.row_base = g->row_base;
+        sa.X = ga.X; sa.ldx = X->ld; sa.Y = ga.Y; sa.ldy = Y->ld;
+        sa.out = ga.alpha; sa.ldo = alpha->ld; sa.H = H; sa.Fh = X->cols / H;
+        e = sa.Fh > 0 ? gsp::launch_sddmm(sa, cs)
+                      : cudaMemset2DAsync(alpha->data, (size_t)alpha->ld * 4, 0, (size_t)H * 4, (size_t)g->E, cs);
+        if (e == cudaSuccess) {
+            gsp::SoftmaxArgs xa{};
+            xa.off = S.off; xa.order = S.order; xa.nrows = S.nrows; xa.n_heavy = S.n_heavy;
+            xa.e = ga.alpha; xa.lde = alpha->ld; xa.out = ga.alpha; xa.ldo = alpha->ld; xa.H = H;
+            e = gsp::launch_softmax(xa, cs);
+        }
+        if (e == cudaSuccess) {
+            gsp::SpmmArgs wa{};
+            wa.off = S.off; wa.col = S.col; wa.order = S.order; wa.nrows = S.nrows; wa.n_heavy = S.n_heavy;
+            wa.X = ga.Vt; wa.ldx = Vt->ld; wa.out = ga.out; wa.ldo = out->ld; wa.F = Vt->cols;
+            wa.w = ga.alpha; wa.ldw = alpha->ld; wa.H = H; wa.Fh = Vt->cols / H > 0 ? Vt->cols / H : 1;
+            e = gsp::launch_spmm(wa, gsp::kSpmmWeightedFwd, cs);
+        }
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "gat_forward launch");
+    return GSP_OK;
+}
+
 // -------------------------------------------------------------- partition
 static void bounds_of(const std::vector<int64_t> &off, int64_t V, int nparts, int64_t *bounds) {
     const int64_t E = off[V];

@@ -72,6 +72,28 @@ struct SoftmaxBwdArgs {
 };
 cudaError_t launch_softmax_bwd(const SoftmaxBwdArgs &a, cudaStream_t s);
 
+// Fused GAT forward: alpha = edge_softmax(gsddmm(X, Y)),
+// out = gspmm_weighted(Vt, alpha), one pass per destination row, alpha still
+// written (state tensor).  Fast path: Fh == 8, H in {2,..,32} power of two.
+struct GatArgs {
+    const int64_t *off;
+    const int32_t *col;
+    const int32_t *order;
+    int64_t nrows, n_heavy, row_base;
+    const float *X;
+    int64_t ldx;
+    const float *Y;
+    int64_t ldy;
+    const float *Vt;
+    int64_t ldv;
+    float *alpha;      // [E, H], ld == H
+    float *out;
+    int64_t ldo;
+    int64_t H;
+};
+bool gat_fused_supported(const GatArgs &a);
+cudaError_t launch_gat_fused(const GatArgs &a, cudaStream_t s);
+
 // fp32 degree scales from (clamped) integer degrees: inv = 1/d^, rsq = d^^-1/2
 // computed in fp64 then rounded once.
 cudaError_t launch_degree_scales(const int64_t *deg, int64_t n, float *inv, float *rsq, cudaStream_t s);

@@ -27,7 +27,7 @@ STATUS = {0: "GSP_OK", 1: "GSP_ERR_NULL", 2: "GSP_ERR_ARG", 3: "GSP_ERR_VERTEX_R
 # the exported C symbols (include/gsp.h), checked by tests/test_abi.py
 SYMBOLS = ["gsp_graph_create", "gsp_graph_destroy", "gsp_graph_info", "gsp_graph_export", "gsp_gspmm",
            "gsp_gspmm_weighted", "gsp_gsddmm", "gsp_edge_softmax", "gsp_edge_softmax_backward",
-           "gsp_partition_bounds", "gsp_graph_partition",
+           "gsp_gat_forward", "gsp_partition_bounds", "gsp_graph_partition",
            "gsp_partition_info", "gsp_status_string", "gsp_last_error_detail", "gsp_version"]
 
 
@@ -61,6 +61,7 @@ def _load():
         "gsp_gsddmm": ([p, T, T, T, p], ci),
         "gsp_edge_softmax": ([p, T, T, p], ci),
         "gsp_edge_softmax_backward": ([p, T, T, T, p], ci),
+        "gsp_gat_forward": ([p, T, T, T, T, T, p], ci),
         "gsp_partition_bounds": ([p, ci, ci, p], ci),
         "gsp_graph_partition": ([p, ci, ci, ci, u32, P(p)], ci),
         "gsp_partition_info": ([p, P(ci), P(ci), P(i64), P(i64), P(i64), P(i64), P(ci)], ci),
@@ -221,6 +222,21 @@ def _edge_softmax_backward(self, alpha, dalpha, out=None, stream=None):
 
 
 Graph.edge_softmax_backward = _edge_softmax_backward
+
+
+def _gat_forward(self, X, Y, Vt, H, alpha=None, out=None, stream=None):
+    """alpha = edge_softmax(gsddmm(X, Y)); out = gspmm_weighted(Vt, alpha) -- fused (NEXT-2)."""
+    if alpha is None:
+        alpha = self._alloc(self.E, H, X)
+    if out is None:
+        out = self._alloc(self.V, Vt.shape[1], X)
+    dx, dy, dv, da, do = _desc(X), _desc(Y), _desc(Vt), _desc(alpha), _desc(out)
+    _check(lib.gsp_gat_forward(self._h, ctypes.byref(dx), ctypes.byref(dy), ctypes.byref(dv), ctypes.byref(da),
+                               ctypes.byref(do), _stream(stream, X.device)))
+    return alpha, out
+
+
+Graph.gat_forward = _gat_forward
 
 
 def version():

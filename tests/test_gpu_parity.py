@@ -406,3 +406,42 @@ def test_softmax_backward_random(gsp, H, ld):
         g = dev(gh)
         G.edge_softmax_backward(dev(ah), g, out=g)                 # in place on dalpha
         assert_within(g.cpu().numpy(), ref, T, f"H{H} in place")
+
+
+# ---------------------------------------------------- NEXT-2: fused GAT forward
+def _gat_check(gsp, V, src, dst, H, Fh, Fv, same, ld=None, seed=0):
+    G, og = graph_pair(gsp, V, src, dst)
+    Xh = datagen.uniform(seed + 1, V, H * Fh)
+    Yh = datagen.uniform(seed + 2, V, H * Fh)
+    Vh = Yh if same else datagen.uniform(seed + 3, V, H * Fv)
+    a_ref, o_ref, T = og.gat_forward(Xh, Yh, Vh, H)
+    X = padded(Xh, ld or H * Fh)
+    Y = dev(Yh)
+    Vt = Y if same else dev(Vh)
+    alpha, out = G.gat_forward(X, Y, Vt, H)
+    # tolerances: alpha 2e-5 absolute, out 2e-5 (T + 1)
+    assert_within(alpha.cpu().numpy(), a_ref, 1.0, f"alpha H{H} Fh{Fh}")
+    assert_within(out.cpu().numpy(), o_ref, T, f"out H{H} Fh{Fh}", scale=2e-5)
+
+
+@pytest.mark.parametrize("H,Fh,Fv,same", [(8, 8, 8, True), (8, 8, 8, False), (2, 8, 8, True), (4, 8, 8, False),
+                                          (16, 8, 8, True), (1, 8, 8, True), (3, 5, 4, False), (8, 4, 8, False)])
+def test_gat_forward_random(gsp, H, Fh, Fv, same):
+    if same and Fv != Fh:
+        return
+    for seed in range(2):
+        rng = np.random.default_rng(seed + 13 * H + Fh)
+        V = int(rng.integers(1, 2500))
+        E = int(rng.integers(0, 30000))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed == 0
+                    else datagen.skewed_multigraph(V, E, seed, alpha=1.6))
+        _gat_check(gsp, V, src, dst, H, Fh, Fv, same, seed=seed)
+
+
+def test_gat_forward_heavy_rows_and_pubmed(gsp):
+    V, E = 3000, 400_000
+    src, dst = datagen.skewed_multigraph(V, E, 21, alpha=1.6)
+    _gat_check(gsp, V, src, dst, 8, 8, 8, True, seed=3)
+    cfg = datagen.CONFIGS["pubmed"]
+    V, src, dst = datagen.make_graph(cfg)
+    _gat_check(gsp, V, src, dst, 8, 8, 8, True, seed=4)

@@ -480,3 +480,28 @@ def test_softmax_backward_closed_forms(golden):
     p = np.float64(np.float32(0.3)); q = np.float64(np.float32(0.7))
     assert ds[0, 0] == pytest.approx(p * (2.0 - (p * 2.0 - q)), abs=1e-15)
     assert ds[0, 0] == pytest.approx(p * q * 3.0, rel=1e-6)
+
+
+# --------------------------------------------------- C10 fused GAT (NEXT-2)
+@pytest.mark.parametrize("seed", range(15))
+def test_gat_forward_is_the_composition(seed):
+    """C10 (fp64 end to end) == C5(C7(C6)) with the pinned components, up to the
+    fp32 hand-off the component interfaces impose; softmax rows sum to 1."""
+    V, src, dst = rand_graph(9000 + seed)
+    G = oracle.Graph(V, src, dst)
+    H = [1, 2, 4][seed % 3]
+    Fh, Fvh = 1 + seed % 3, 2
+    X = datagen.uniform(seed, V, H * Fh)
+    Y = datagen.uniform(seed + 1, V, H * Fh)
+    Vt = datagen.uniform(seed + 2, V, H * Fvh)
+    a, out, T = G.gat_forward(X, Y, Vt, H)
+    s, _ = G.gsddmm(X, Y, H)
+    a2 = G.edge_softmax(s.astype(np.float32))
+    assert np.allclose(a, a2, atol=2e-6)
+    o2, T2 = G.gspmm_weighted(Vt, a2.astype(np.float32))
+    assert np.all(np.abs(out - o2) <= 1e-5 * (T + 1))
+    rows = np.repeat(np.arange(V), np.diff(G.fwd_off))
+    sums = np.zeros((V, H))
+    np.add.at(sums, rows, a)
+    nz = np.diff(G.fwd_off) > 0
+    assert np.allclose(sums[nz], 1.0, atol=1e-13)

@@ -8,7 +8,7 @@ import datagen, paper_2402_03548_b200 as gsp
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="reddit")
 ap.add_argument("--reps", type=int, default=10)
-ap.add_argument("--ops", default="gspmm_fwd,gspmm_rev,gsddmm,edge_softmax,wfwd,wrev")
+ap.add_argument("--ops", default="gspmm_fwd,gspmm_rev,gsddmm,edge_softmax,wfwd,wrev,gat_fused,softmax_bwd")
 ap.add_argument("--F", type=int, default=0)
 ap.add_argument("--ld", type=int, default=0)
 ap.add_argument("--tag", default=os.environ.get("GSP_TUNE_SPMM", ""))
@@ -26,6 +26,7 @@ Z = torch.from_numpy(datagen.uniform(2, V, Fg)).cuda()
 out = torch.empty((V, F), device="cuda")
 outg = torch.empty((V, Fg), device="cuda")
 s = torch.empty((E, H), device="cuda")
+s2 = torch.rand((E, H), device="cuda")
 flush = torch.empty(512 << 18, device="cuda")
 ops = {
     "gspmm_fwd": lambda: G.gspmm(X, 2, out=out),
@@ -34,6 +35,8 @@ ops = {
     "edge_softmax": lambda: G.edge_softmax(s, out=s),
     "wfwd": lambda: G.gspmm_weighted(Z, s, out=outg),
     "wrev": lambda: G.gspmm_weighted(Z, s, out=outg, reverse=True),
+    "gat_fused": lambda: G.gat_forward(Z, Z, Z, H, alpha=s, out=outg),
+    "softmax_bwd": lambda: G.edge_softmax_backward(s, s2, out=s2),
 }
 G.gsddmm(Z, Z, out=s); G.edge_softmax(s, out=s)
 res = {}
