@@ -401,6 +401,38 @@ def main_gsp(args):
     peak, peak_kind = load_peaks()
     avg = {k: (sum(v) / len(v) if v else None) for k, v in ev.items()}
     Vloc, Eloc = (R, Ep) if P > 1 else (V, E)
+    # ------------------------------------------- NEXT rows (outside the step)
+    next_rows = None
+    if not args.profile:
+        def time_op(fn, reps=5):
+            for _ in range(2):
+                fn()
+            ts = []
+            for _ in range(reps):
+                flush.fill_(1.0)
+                a0 = torch.cuda.Event(enable_timing=True)
+                a1 = torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                fn()
+                a1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a0.elapsed_time(a1))
+            return sorted(ts)[len(ts) // 2]
+        alpha2 = torch.empty((Ep, H), device="cuda")
+        gout = torch.empty((R, F), device="cuda")
+        dal = torch.rand((Ep, H), device="cuda")
+        ms_gat = time_op(lambda: part.gat_forward(Z, Z, Z, H, alpha=alpha2, out=gout, stream=stream))
+        ms_sbw = time_op(lambda: part.edge_softmax_backward(s, dal, out=dal, stream=stream))
+        sep = avg["gsddmm"] + avg["edge_softmax"] + avg["gspmm_weighted_fwd"]
+        next_rows = {
+            "gat_forward_fused": {"row": "NEXT-2", "ms": round(ms_gat, 4),
+                                  "vs_separate_chain_ms": round(sep, 4),
+                                  "GE_s": round(Eloc / (ms_gat * 1e-3) / 1e9, 3)},
+            "edge_softmax_backward": {"row": "NEXT-1", "ms": round(ms_sbw, 4),
+                                      "GB_s": round(alg_bytes("edge_softmax", Vloc, Eloc, F, H) * 1.5 / (ms_sbw * 1e-3) / 1e9, 1)},
+        }
+        del alpha2, gout, dal
+
     per_op = {}
     bytes_of = {"gspmm_fwd": alg_bytes("gspmm", Vloc, Eloc, F, H), "gspmm_rev": alg_bytes("gspmm", Vloc, Eloc, F, H),
                 "gsddmm": alg_bytes("gsddmm", Vloc, Eloc, F, H),
@@ -451,6 +483,7 @@ def main_gsp(args):
             "per_op": per_op,
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "next_rows": next_rows,
             "e2e": e2e,
             "gpu_launches": (6 * args.steps),
             "clocks": clk,
