@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.h"
 
@@ -709,9 +710,13 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
     constexpr int VEC = 8;
     constexpr int G = 32 / LPE;
     constexpr int PER = LPE;
-    constexpr int U = PER >= 4 ? 4 : PER;   // edges in flight per lane
+    constexpr int U = SAME ? (PER >= 8 ? 8 : PER) : (PER >= 4 ? 4 : PER);   // edges in flight per lane
     __shared__ __align__(16) int s_col[kWarps][32];
-    __shared__ float sm_state[kWarps][LPE][VEC + 2];   // heavy rows: per-warp (m, S, acc[8]) per head
+    // running Kahan state (acc, accc) per lane lives in smem: touched once per
+    // tile (fold) and on the rare max increase (rescale), keeping registers for
+    // the gathers in flight.  Reused for the heavy-row cross-warp merge.
+    __shared__ __align__(16) float s_run[kWarps][32][2 * VEC];
+    __shared__ float sm_ms[kWarps][LPE][2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / LPE, h = lane % LPE;   // head of this lane
     const int H = LPE;
@@ -727,15 +732,14 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
     const char *vl = reinterpret_cast<const char *>(a.Vt + h * VEC);
     const uint32_t ldyb = (uint32_t)(a.ldy * 4), ldvb = (uint32_t)(a.ldv * 4);
 
-    // running (m, S, acc) with Kahan compensation (Sc, accc) folded once per
-    // 32-edge tile from the tile-local sums (St, acct) -- error independent of
-    // the row length; a rescale (new max)
-    // multiplies all of them by the same factor.
+    // (m, S + Sc compensation) in registers; acc / accc in smem; tile sums in registers
     float m = -INFINITY, S = 0.f, Sc = 0.f, St = 0.f;
-    Vec<VEC> acc, accc, acct;
-    vzero(acc);
-    vzero(accc);
+    float *run = s_run[warp][lane];
+#pragma unroll
+    for (int t = 0; t < 2 * VEC; t++) run[t] = 0.f;
+    Vec<VEC> acct;
     vzero(acct);
+    int ntile = 0;
 
     auto load_col = [&](int64_t tb) { return tb + lane < e ? ld_stream_i32(a.col + tb + lane, pol.stream) : 0; };
     int c1 = load_col(b), c2 = load_col(b + 32);
@@ -748,65 +752,101 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
         const int *gp = &s_col[warp][g * PER];
         float *ab = a.alpha + (base + g) * H + h;   // group g's i-th edge is tile edge g + G*i
         const int mcount = n == 32 ? PER : (n > g ? (n - g + G - 1) / G : 0);
-#pragma unroll 1
-        for (int i = 0; i < mcount; i += U) {
+        auto body = [&](int i, auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
             Vec<VEC> y[U], vv[SAME ? 1 : U];
+            int cc[U];
+            if constexpr (U % 4 == 0) {
+#pragma unroll
+                for (int u = 0; u < U; u += 4) {
+                    const int4 c4 = *reinterpret_cast<const int4 *>(gp + i + u);
+                    cc[u] = c4.x; cc[u + 1] = c4.y; cc[u + 2] = c4.z; cc[u + 3] = c4.w;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; u++) cc[u] = gp[i + u];
+            }
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                if (i + u < mcount) {
-                    const int c = gp[i + u];
-                    ld_keep(y[u], reinterpret_cast<const float *>(yl + (uint64_t)(uint32_t)c * ldyb), pol.keep);
+                if (FULL || i + u < mcount) {
+                    ld_keep(y[u], reinterpret_cast<const float *>(yl + (uint64_t)(uint32_t)cc[u] * ldyb), pol.keep);
                     if constexpr (!SAME)
-                        ld_keep(vv[u], reinterpret_cast<const float *>(vl + (uint64_t)(uint32_t)c * ldvb), pol.keep);
+                        ld_keep(vv[u], reinterpret_cast<const float *>(vl + (uint64_t)(uint32_t)cc[u] * ldvb), pol.keep);
                 } else {
                     vzero(y[u]);
                     if constexpr (!SAME) vzero(vv[u]);
                 }
             }
+            // scores of the batch, at most one rescale per batch, then the weights
+            float sc[U];
+            float mb = -INFINITY;
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                if (i + u < mcount) {
-                    float sc = 0.f;
+                float s0 = 0.f, s1 = 0.f;   // two chains: shorter dependency
 #pragma unroll
-                    for (int t = 0; t < VEC; t++) sc = fmaf(xv.v[t], y[u].v[t], sc);
-                    ab[(int64_t)(G * (i + u)) * H] = sc;   // raw score (default L2 policy), re-read below
-                    const Vec<VEC> &val = SAME ? y[u] : vv[SAME ? 0 : u];
-                    if (sc > m) {
-                        const float r = fast_exp(m - sc);   // 0 when m = -inf
-                        S *= r; Sc *= r; St = St * r + 1.f;
-#pragma unroll
-                        for (int t = 0; t < VEC; t++) {
-                            acc.v[t] *= r;
-                            accc.v[t] *= r;
-                            acct.v[t] = fmaf(acct.v[t], r, val.v[t]);
-                        }
-                        m = sc;
-                    } else {
-                        const float p = fast_exp(sc - m);
-                        St += p;
-#pragma unroll
-                        for (int t = 0; t < VEC; t++) acct.v[t] = fmaf(p, val.v[t], acct.v[t]);
-                    }
+                for (int t = 0; t < VEC; t += 2) {
+                    s0 = fmaf(xv.v[t], y[u].v[t], s0);
+                    s1 = fmaf(xv.v[t + 1], y[u].v[t + 1], s1);
+                }
+                sc[u] = s0 + s1;
+                if (FULL || i + u < mcount) {
+                    ab[(int64_t)(G * (i + u)) * H] = sc[u];   // raw score (default L2 policy), re-read below
+                    mb = fmaxf(mb, sc[u]);
+                } else {
+                    sc[u] = -INFINITY;
                 }
             }
+            // lazy rescale: the reference m moves only when a score exceeds it by
+            // more than 8 (exp(s - m) <= e^8 keeps every sum finite); the result
+            // exp(s - m) / sum exp(s - m) does not depend on the reference, and the
+            // (warp-divergent) branch is taken about once per row.
+            if (mb > m + 8.f) {
+                const float r = fast_exp(m - mb);   // 0 when m = -inf
+                S *= r; Sc *= r; St *= r;
+#pragma unroll
+                for (int t = 0; t < VEC; t++) {
+                    run[t] *= r;
+                    run[VEC + t] *= r;
+                    acct.v[t] *= r;
+                }
+                m = mb;
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const float pu = fast_exp(sc[u] - m);   // 0 for padding (-inf)
+                const Vec<VEC> &val = SAME ? y[u] : vv[SAME ? 0 : u];
+                St += pu;
+#pragma unroll
+                for (int t = 0; t < VEC; t++) acct.v[t] = fmaf(pu, val.v[t], acct.v[t]);
+            }
+        };
+        if (n == 32) {
+#pragma unroll 1
+            for (int i = 0; i < PER; i += U) body(i, std::true_type{});
+        } else {
+#pragma unroll 1
+            for (int i = 0; i < mcount; i += U) body(i, std::false_type{});
         }
         __syncwarp();
-        {   // Kahan fold of the tile sums
-            float y = St - Sc, t2 = S + y;
-            Sc = (t2 - S) - y; S = t2; St = 0.f;
+        if (++ntile == kFoldTiles || base + 32 >= e) {   // Kahan fold of the tile sums
+            ntile = 0;
+            float y2 = St - Sc, t2 = S + y2;
+            Sc = (t2 - S) - y2; S = t2; St = 0.f;
 #pragma unroll
             for (int t = 0; t < VEC; t++) {
-                y = acct.v[t] - accc.v[t];
-                t2 = acc.v[t] + y;
-                accc.v[t] = (t2 - acc.v[t]) - y;
-                acc.v[t] = t2;
+                const float ac = run[t], cc = run[VEC + t];
+                y2 = acct.v[t] - cc;
+                t2 = ac + y2;
+                run[VEC + t] = (t2 - ac) - y2;
+                run[t] = t2;
                 acct.v[t] = 0.f;
             }
         }
     }
     S -= Sc;
+    Vec<VEC> acc;
 #pragma unroll
-    for (int t = 0; t < VEC; t++) acc.v[t] -= accc.v[t];
+    for (int t = 0; t < VEC; t++) acc.v[t] = run[t] - run[VEC + t];
     // merge the G edge groups (same head h): online-softmax merge
     auto merge = [&](float mo, float So, const Vec<VEC> &ao) {
         const float mn = fmaxf(m, mo);
@@ -827,11 +867,12 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
     }
     if (heavy) {
         // every warp of the CTA holds (m, S, acc) of its slice per head: merge in warp order
+        __syncthreads();   // s_run is reused for the cross-warp state
         if (g == 0) {
-            sm_state[warp][h][0] = m;
-            sm_state[warp][h][1] = S;
+            sm_ms[warp][h][0] = m;
+            sm_ms[warp][h][1] = S;
 #pragma unroll
-            for (int t = 0; t < VEC; t++) sm_state[warp][h][2 + t] = acc.v[t];
+            for (int t = 0; t < VEC; t++) s_run[warp][h][t] = acc.v[t];
         }
         __syncthreads();
         m = -INFINITY;
@@ -840,8 +881,8 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
         for (int w = 0; w < kWarps; w++) {
             Vec<VEC> ao;
 #pragma unroll
-            for (int t = 0; t < VEC; t++) ao.v[t] = sm_state[w][h][2 + t];
-            merge(sm_state[w][h][0], sm_state[w][h][1], ao);
+            for (int t = 0; t < VEC; t++) ao.v[t] = s_run[w][h][t];
+            merge(sm_ms[w][h][0], sm_ms[w][h][1], ao);
         }
     }
     const float rS = S > 0.f ? 1.0f / S : 0.f;
