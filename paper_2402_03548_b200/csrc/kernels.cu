@@ -940,10 +940,21 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const SoftmaxBwdA
     const Pol pol = make_pol();
     const int64_t lo = b * H, hi = e * H;
     float d[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int64_t i = lo + (int64_t)lane * 4; i < hi; i += 128) {
-        const float4 x = ld_f4(a.alpha + i, pol.keep), y = ld_f4(a.dalpha + i, pol.keep);
-        d[0] = fmaf(x.x, y.x, d[0]); d[1] = fmaf(x.y, y.y, d[1]);
-        d[2] = fmaf(x.z, y.z, d[2]); d[3] = fmaf(x.w, y.w, d[3]);
+    constexpr int NU = 4;   // loads in flight per lane
+    for (int64_t i0 = lo + (int64_t)lane * 4; i0 < hi; i0 += 128 * NU) {
+        float4 x[NU], y[NU];
+#pragma unroll
+        for (int k = 0; k < NU; k++)
+            if (i0 + 128 * k < hi) {
+                x[k] = ld_f4(a.alpha + i0 + 128 * k, pol.keep);
+                y[k] = ld_f4(a.dalpha + i0 + 128 * k, pol.keep);
+            }
+#pragma unroll
+        for (int k = 0; k < NU; k++)
+            if (i0 + 128 * k < hi) {
+                d[0] = fmaf(x[k].x, y[k].x, d[0]); d[1] = fmaf(x[k].y, y[k].y, d[1]);
+                d[2] = fmaf(x[k].z, y[k].z, d[2]); d[3] = fmaf(x[k].w, y[k].w, d[3]);
+            }
     }
 #pragma unroll
     for (int t = 0; t < 4; t++)
@@ -961,10 +972,21 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const SoftmaxBwdA
             d[t] = acc;
         }
     }
-    for (int64_t i = lo + (int64_t)lane * 4; i < hi; i += 128) {
-        const float4 x = ld_f4(a.alpha + i, pol.stream), y = ld_f4(a.dalpha + i, pol.stream);
-        st_stream_f4(a.out + i, make_float4(x.x * (y.x - d[0]), x.y * (y.y - d[1]), x.z * (y.z - d[2]),
-                                            x.w * (y.w - d[3])), pol.stream);
+    for (int64_t i0 = lo + (int64_t)lane * 4; i0 < hi; i0 += 128 * NU) {
+        float4 x[NU], y[NU];
+#pragma unroll
+        for (int k = 0; k < NU; k++)
+            if (i0 + 128 * k < hi) {
+                x[k] = ld_f4(a.alpha + i0 + 128 * k, pol.stream);
+                y[k] = ld_f4(a.dalpha + i0 + 128 * k, pol.stream);
+            }
+#pragma unroll
+        for (int k = 0; k < NU; k++)
+            if (i0 + 128 * k < hi)
+                st_stream_f4(a.out + i0 + 128 * k,
+                             make_float4(x[k].x * (y[k].x - d[0]), x[k].y * (y[k].y - d[1]), x[k].z * (y[k].z - d[2]),
+                                         x[k].w * (y[k].w - d[3])),
+                             pol.stream);
     }
 }
 
