@@ -422,16 +422,24 @@ def main_gsp(args):
         gout = torch.empty((R, F), device="cuda")
         dal = torch.rand((Ep, H), device="cuda")
         ms_gat = time_op(lambda: part.gat_forward(Z, Z, Z, H, alpha=alpha2, out=gout, stream=stream))
+        ms_max = time_op(lambda: part.gspmm_reduce(X, gsp.REDUCE_MAX, out=gout, stream=stream))
+        hout = torch.empty((R, H), device="cuda")
+        ms_e = time_op(lambda: part.gspmm_e(s, gsp.REDUCE_SUM, out=hout, stream=stream))
+        ms_ve = time_op(lambda: part.gsddmm_ve(Z[:, :H], dal, gsp.OP_ADD, gsp.SIDE_SRC, out=alpha2, stream=stream))
         ms_sbw = time_op(lambda: part.edge_softmax_backward(s, dal, out=dal, stream=stream))
         sep = avg["gsddmm"] + avg["edge_softmax"] + avg["gspmm_weighted_fwd"]
         next_rows = {
             "gat_forward_fused": {"row": "NEXT-2", "ms": round(ms_gat, 4),
                                   "vs_separate_chain_ms": round(sep, 4),
                                   "GE_s": round(Eloc / (ms_gat * 1e-3) / 1e9, 3)},
+            "gspmm_reduce_max": {"row": "NEXT-3", "ms": round(ms_max, 4),
+                                 "GB_s": round(alg_bytes("gspmm", Vloc, Eloc, F, H) / (ms_max * 1e-3) / 1e9, 1)},
+            "gspmm_e_sum": {"row": "NEXT-3", "ms": round(ms_e, 4)},
+            "gsddmm_ve_add_src": {"row": "NEXT-3", "ms": round(ms_ve, 4)},
             "edge_softmax_backward": {"row": "NEXT-1", "ms": round(ms_sbw, 4),
                                       "GB_s": round(alg_bytes("edge_softmax", Vloc, Eloc, F, H) * 1.5 / (ms_sbw * 1e-3) / 1e9, 1)},
         }
-        del alpha2, gout, dal
+        del alpha2, gout, dal, hout
 
     per_op = {}
     bytes_of = {"gspmm_fwd": alg_bytes("gspmm", Vloc, Eloc, F, H), "gspmm_rev": alg_bytes("gspmm", Vloc, Eloc, F, H),

@@ -185,6 +185,36 @@ gsp_status gsp_edge_softmax_backward(const gsp_graph *g, const gsp_tensor *alpha
 gsp_status gsp_gat_forward(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *Y, const gsp_tensor *Vt,
                            gsp_tensor *alpha, gsp_tensor *out, gsp_stream stream);
 
+/* ---------------------------------------- Table 1 surface (NEXT-3, §8(f)) */
+enum { GSP_REDUCE_SUM = 0, GSP_REDUCE_MIN = 1, GSP_REDUCE_MAX = 2 };
+enum { GSP_OP_ADD = 0, GSP_OP_SUB = 1, GSP_OP_MUL = 2, GSP_OP_DIV = 3 };
+enum { GSP_SIDE_DST = 0, GSP_SIDE_SRC = 1 };
+
+/* gSpMMv with a reduction ("reduction operation type, such as
+ * sum, min, max"), no normalisation (norm only with sum):
+ *   reverse = 0: out[v,f] = RED_{j in fwd row v} X[col_j, f]   (rev: over rev row u)
+ * Empty rows -> 0.  reduce = SUM is gsp_gspmm(norm = NONE).
+ * Shapes / errors as gsp_gspmm; ARG for an unknown reduce. */
+gsp_status gsp_gspmm_reduce(const gsp_graph *g, const gsp_tensor *X, int reduce, gsp_tensor *out, int reverse,
+                            gsp_stream stream);
+
+/* gSpMMe / gSpMMeid: an edge tensor reduced per row, fetched
+ * through the edge ID:  reverse = 0: out[v,h] = RED_{j in fwd row v} w[j,h];
+ * reverse = 1: out[u,h] = RED_{k in rev row u} w[rev_eid_k, h].  w [E,H] by
+ * edge ID, out [nrows, H] (fwd partitions, reverse = 1: [ncols, H] partials
+ * over the partition's own edges, as gsp_gspmm_weighted).  Empty rows -> 0;
+ * sums accumulate in fp64.  Errors as gsp_gspmm_weighted. */
+gsp_status gsp_gspmm_e(const gsp_graph *g, const gsp_tensor *w, int reduce, gsp_tensor *out, int reverse,
+                       gsp_stream stream);
+
+/* gSDDMMve: for slot j of fwd row v with
+ * column u,  out[j,h] = w[j,h] OP X[side == GSP_SIDE_SRC ? u : v, h].
+ * X [ncols, H] (partitions: the padded table), w/out [E, H]; out == w exactly
+ * is allowed (in place).  Additive GAT scores e = a_dst[v] + a_src[u] are two
+ * calls: (w = 0) ADD DST, then in place ADD SRC.  IEEE semantics for DIV. */
+gsp_status gsp_gsddmm_ve(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *w, int op, int side,
+                         gsp_tensor *out, gsp_stream stream);
+
 /* -------------------------------------------------------------- multi-GPU */
 
 /* Edge-balanced contiguous row bounds:

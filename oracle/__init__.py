@@ -22,6 +22,8 @@ _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.c")
 
 NORM_NONE, NORM_RIGHT, NORM_BOTH = 0, 1, 2
+RED_SUM, RED_MIN, RED_MAX = 0, 1, 2
+OP_ADD, OP_SUB, OP_MUL, OP_DIV = 0, 1, 2, 3
 
 
 def build(force: bool = False) -> str:
@@ -60,6 +62,12 @@ def _L():
         lib.oracle_edge_softmax_backward.restype = ci
         lib.oracle_gat_forward.argtypes = [i64, p, p, p, i64, p, i64, i64, p, i64, i64, i64, p, p, p, p]
         lib.oracle_gat_forward.restype = ci
+        lib.oracle_gspmm_reduce.argtypes = [i64, p, p, p, p, p, i64, i64, ci, ci, p, p]
+        lib.oracle_gspmm_reduce.restype = ci
+        lib.oracle_gspmm_e.argtypes = [i64, p, p, p, p, i64, ci, ci, p, p]
+        lib.oracle_gspmm_e.restype = ci
+        lib.oracle_gsddmm_ve.argtypes = [i64, p, p, p, p, i64, ci, ci, p]
+        lib.oracle_gsddmm_ve.restype = ci
         lib.oracle_partition_bounds.argtypes = [i64, p, i64, p]
         lib.oracle_partition_bounds.restype = ci
         lib.oracle_partition_structure.argtypes = [i64, p, p, i64, p, i64, p, p]
@@ -207,6 +215,38 @@ class Graph:
                                      _ptr(scratch))
         assert rc == 0, rc
         return alpha, out, T
+
+    # --- C11-C13 (NEXT-3)
+    def gspmm_reduce(self, X, red, reverse=False):
+        X = _c(X, np.float32)
+        F = X.shape[1]
+        out = np.empty((self.V, F), np.float64)
+        T = np.empty((self.V, F), np.float64)
+        rc = _L().oracle_gspmm_reduce(self.V, _ptr(self.fwd_off), _ptr(self.fwd_col), _ptr(self.rev_off),
+                                      _ptr(self.rev_col), _ptr(X), F, F, red, int(bool(reverse)), _ptr(out), _ptr(T))
+        assert rc == 0, rc
+        return out, T
+
+    def gspmm_e(self, w, red, reverse=False):
+        w = _c(w, np.float32)
+        H = w.shape[1]
+        out = np.empty((self.V, H), np.float64)
+        T = np.empty((self.V, H), np.float64)
+        rc = _L().oracle_gspmm_e(self.V, _ptr(self.fwd_off), _ptr(self.rev_off), _ptr(self.rev_eid), _ptr(w), H,
+                                 red, int(bool(reverse)), _ptr(out), _ptr(T))
+        assert rc == 0, rc
+        return out, T
+
+    def gsddmm_ve(self, X, w, op, side_src):
+        X = _c(X, np.float32)
+        w = _c(w, np.float32)
+        H = w.shape[1]
+        assert X.shape[1] == H
+        out = np.empty((self.E, H), np.float64)
+        rc = _L().oracle_gsddmm_ve(self.V, _ptr(self.fwd_off), _ptr(self.fwd_col), _ptr(X), _ptr(w), H, op,
+                                   int(bool(side_src)), _ptr(out))
+        assert rc == 0, rc
+        return out
 
     # --- C8
     def partition_bounds(self, nparts, reverse=False):

@@ -318,6 +318,83 @@ int oracle_gat_forward(int64_t V, const int64_t *fwd_off, const int32_t *fwd_col
     return 0;
 }
 
+/* ----------------------------------------------------------- C11-C13 --- */
+/* Table 1's remaining API surface:
+ * reductions sum / min / max ("various reduction operations (e.g. sum,
+ * min, max"), empty rows -> 0 (SPEC S:237 design decision). */
+enum { OR_RED_SUM = 0, OR_RED_MIN = 1, OR_RED_MAX = 2 };
+static double red_init(int r) { return r == OR_RED_MIN ? INFINITY : (r == OR_RED_MAX ? -INFINITY : 0.0); }
+static double red_apply(int r, double acc, double x) {
+    if (r == OR_RED_MIN) return x < acc ? x : acc;
+    if (r == OR_RED_MAX) return x > acc ? x : acc;
+    return acc + x;
+}
+
+/* C11 gSpMMv with a reduction ("gSpMMv(g, in, out, eFn, Flag)"
+ * "reduction operation type, such as sum, min, max"), no normalisation:
+ *   fwd: out[v,f] = RED_{j in fwd row v} X[fwd_col[j], f];  rev: over rev row u of X[rev_col[k], f]. */
+int oracle_gspmm_reduce(int64_t V, const int64_t *fwd_off, const int32_t *fwd_col, const int64_t *rev_off,
+                        const int32_t *rev_col, const float *X, int64_t F, int64_t ldx, int red, int reverse,
+                        double *out, double *T) {
+    const int64_t *off = reverse ? rev_off : fwd_off;
+    const int32_t *col = reverse ? rev_col : fwd_col;
+    for (int64_t v = 0; v < V; v++)
+        for (int64_t f = 0; f < F; f++) {
+            double acc = red_init(red), tacc = 0.0;
+            for (int64_t j = off[v]; j < off[v + 1]; j++) {
+                double x = (double)X[(int64_t)col[j] * ldx + f];
+                acc = red_apply(red, acc, x);
+                tacc += fabs(x);
+            }
+            out[v * F + f] = off[v] == off[v + 1] ? 0.0 : acc;
+            if (T) T[v * F + f] = red == OR_RED_SUM ? tacc : 0.0;   /* min / max are exact */
+        }
+    return 0;
+}
+
+/* C12 gSpMMe / gSpMMeid ("gSpMMeid(g, in, out, eFn, Flag)"): an
+ * edge-level tensor reduced per row, fetched through the edge ID:
+ *   fwd: out[v,h] = RED_{j in fwd row v} w[j, h];  rev: out[u,h] = RED_{k in rev row u} w[rev_eid[k], h]. */
+int oracle_gspmm_e(int64_t V, const int64_t *fwd_off, const int64_t *rev_off, const int32_t *rev_eid,
+                   const float *w, int64_t H, int red, int reverse, double *out, double *T) {
+    for (int64_t v = 0; v < V; v++)
+        for (int64_t h = 0; h < H; h++) {
+            double acc = red_init(red), tacc = 0.0;
+            int64_t b = reverse ? rev_off[v] : fwd_off[v], e = reverse ? rev_off[v + 1] : fwd_off[v + 1];
+            for (int64_t k = b; k < e; k++) {
+                int64_t eid = reverse ? rev_eid[k] : k;
+                double x = (double)w[eid * H + h];
+                acc = red_apply(red, acc, x);
+                tacc += fabs(x);
+            }
+            out[v * H + h] = b == e ? 0.0 : acc;
+            if (T) T[v * H + h] = red == OR_RED_SUM ? tacc : 0.0;
+        }
+    return 0;
+}
+
+/* C13 gSDDMMve ("gSDDMMve(g, in, in, out, eFn, Flag)"
+ * "vertex-level and edge-level tensors are accessed using the graph"; SPEC
+ * S:199-207): for slot j of fwd row v with column u,
+ *   out[j,h] = w[j,h] OP X[side ? u : v, h],  OP in {add, sub, mul, div}. */
+enum { OR_OP_ADD = 0, OR_OP_SUB = 1, OR_OP_MUL = 2, OR_OP_DIV = 3 };
+int oracle_gsddmm_ve(int64_t V, const int64_t *fwd_off, const int32_t *fwd_col, const float *X, const float *w,
+                     int64_t H, int op, int side_src, double *out) {
+    for (int64_t v = 0; v < V; v++)
+        for (int64_t j = fwd_off[v]; j < fwd_off[v + 1]; j++) {
+            int64_t vx = side_src ? fwd_col[j] : v;
+            for (int64_t h = 0; h < H; h++) {
+                double a = (double)w[j * H + h], x = (double)X[vx * H + h], r;
+                if (op == OR_OP_ADD) r = a + x;
+                else if (op == OR_OP_SUB) r = a - x;
+                else if (op == OR_OP_MUL) r = a * x;
+                else r = a / x;
+                out[j * H + h] = r;
+            }
+        }
+    return 0;
+}
+
 /* ------------------------------------------------------------------ C8 --- */
 /* Edge-balanced contiguous row partition (BJ north_star
  * "destination-row partitioner"):  b_0 = 0, b_P = V,

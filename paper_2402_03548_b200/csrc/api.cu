@@ -550,6 +550,88 @@ gsp_status gsp_gat_forward(const gsp_graph *g, const gsp_tensor *X, const gsp_te
     return GSP_OK;
 }
 
+// ------------------------------------------------ NEXT-3: Table 1 surface
+gsp_status gsp_gspmm_reduce(const gsp_graph *g, const gsp_tensor *X, int reduce, gsp_tensor *out, int reverse,
+                            gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    if (reduce < GSP_REDUCE_SUM || reduce > GSP_REDUCE_MAX) return fail(GSP_ERR_ARG, "reduce must be 0, 1 or 2");
+    if (reduce == GSP_REDUCE_SUM) return gsp_gspmm(g, X, GSP_NORM_NONE, out, reverse, stream);
+    if (reverse != 0 && reverse != 1) return fail(GSP_ERR_ARG, "reverse must be 0 or 1");
+    const gsp::DevStructure &S = reverse ? g->rev : g->fwd;
+    if (!S.present)
+        return reverse ? fail(GSP_ERR_NO_REVERSE, "graph has no rev structure (GSP_BUILD_REVERSE)")
+                       : fail(GSP_ERR_ARG, "this partition only serves reverse = 1");
+    if (!X || !out) return fail(GSP_ERR_NULL, "X/out is NULL");
+    if ((st = check_tensor(g, X, "X", S.ncols, -1)) != GSP_OK) return st;
+    if ((st = check_tensor(g, out, "out", S.nrows, X->cols)) != GSP_OK) return st;
+    if (overlaps(X, out)) return fail(GSP_ERR_ALIAS, "out overlaps X");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    gsp::SpmmArgs a{};
+    a.off = S.off; a.col = S.col; a.order = S.order; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
+    a.out = static_cast<float *>(out->data); a.ldo = out->ld;
+    a.F = X->cols; a.H = 1; a.Fh = X->cols > 0 ? X->cols : 1;
+    cudaError_t e = gsp::launch_spmm(a, reduce == GSP_REDUCE_MIN ? gsp::kSpmmMin : gsp::kSpmmMax, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gspmm_reduce launch");
+    return GSP_OK;
+}
+
+gsp_status gsp_gspmm_e(const gsp_graph *g, const gsp_tensor *w, int reduce, gsp_tensor *out, int reverse,
+                       gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    if (reduce < GSP_REDUCE_SUM || reduce > GSP_REDUCE_MAX) return fail(GSP_ERR_ARG, "reduce must be 0, 1 or 2");
+    if (reverse != 0 && reverse != 1) return fail(GSP_ERR_ARG, "reverse must be 0 or 1");
+    const gsp::DevStructure &S = reverse ? (g->is_partition ? g->lrev : g->rev) : g->fwd;
+    if (!S.present || (reverse && !S.eid))
+        return reverse ? fail(GSP_ERR_NO_REVERSE, "no rev structure with edge ids on this graph")
+                       : fail(GSP_ERR_ARG, "this partition only serves reverse = 1");
+    if (!w || !out) return fail(GSP_ERR_NULL, "w/out is NULL");
+    if ((st = check_tensor(g, w, "w", g->E, -1)) != GSP_OK) return st;
+    if ((st = check_tensor(g, out, "out", S.nrows, w->cols)) != GSP_OK) return st;
+    if (overlaps(w, out)) return fail(GSP_ERR_ALIAS, "out overlaps w");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    gsp::SpmmEArgs a{};
+    a.off = S.off; a.eid = reverse ? S.eid : nullptr; a.order = S.order; a.nrows = S.nrows;
+    a.w = static_cast<const float *>(w->data); a.ldw = w->ld;
+    a.out = static_cast<float *>(out->data); a.ldo = out->ld;
+    a.H = w->cols; a.red = reduce;
+    cudaError_t e = gsp::launch_spmm_e(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gspmm_e launch");
+    return GSP_OK;
+}
+
+gsp_status gsp_gsddmm_ve(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *w, int op, int side,
+                         gsp_tensor *out, gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    if (op < GSP_OP_ADD || op > GSP_OP_DIV) return fail(GSP_ERR_ARG, "op must be 0..3");
+    if (side != GSP_SIDE_DST && side != GSP_SIDE_SRC) return fail(GSP_ERR_ARG, "side must be 0 or 1");
+    const gsp::DevStructure &S = g->fwd;
+    if (!S.present) return fail(GSP_ERR_ARG, "gsddmm_ve needs the fwd structure (not a reverse partition)");
+    if (!X || !w || !out) return fail(GSP_ERR_NULL, "X/w/out is NULL");
+    if ((st = check_tensor(g, w, "w", g->E, -1)) != GSP_OK) return st;
+    if ((st = check_tensor(g, X, "X", S.ncols, w->cols)) != GSP_OK) return st;
+    if ((st = check_tensor(g, out, "out", g->E, w->cols)) != GSP_OK) return st;
+    if (overlaps(X, out)) return fail(GSP_ERR_ALIAS, "out overlaps X");
+    const bool same = w->data == out->data && w->ld == out->ld;
+    if (!same && overlaps(w, out)) return fail(GSP_ERR_ALIAS, "out partially overlaps w");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    gsp::SddmmVeArgs a{};
+    a.off = S.off; a.col = S.col; a.order = S.order; a.nrows = S.nrows; a.row_base = g->row_base;
+    a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
+    a.w = static_cast<const float *>(w->data); a.ldw = w->ld;
+    a.out = static_cast<float *>(out->data); a.ldo = out->ld;
+    a.H = w->cols; a.op = op; a.side_src = side;
+    cudaError_t e = gsp::launch_sddmm_ve(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gsddmm_ve launch");
+    return GSP_OK;
+}
+
 // -------------------------------------------------------------- partition
 static void bounds_of(const std::vector<int64_t> &off, int64_t V, int nparts, int64_t *bounds) {
     const int64_t E = off[V];

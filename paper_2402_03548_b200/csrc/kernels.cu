@@ -181,7 +181,14 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     constexpr int U0 = UOVR ? UOVR : (UB < 2 ? 2 : (UB > 4 ? 4 : UB));
     constexpr int U = U0 > PER ? PER : U0;
     constexpr int SW = VEC * LPE * CPL;   // feature slab handled by this CTA
-    constexpr bool W = MODE != kSpmmScaled;
+    constexpr bool W = MODE == kSpmmWeightedFwd || MODE == kSpmmWeightedRev;
+    constexpr bool MM = MODE == kSpmmMin || MODE == kSpmmMax;   // min / max reductions (NEXT-3)
+    constexpr float ID = MODE == kSpmmMin ? INFINITY : (MODE == kSpmmMax ? -INFINITY : 0.f);
+    auto comb = [](float x, float y) {
+        if constexpr (MODE == kSpmmMin) return fminf(x, y);
+        else if constexpr (MODE == kSpmmMax) return fmaxf(x, y);
+        else return x + y;
+    };
     constexpr int RED = kWarps * SW;
     constexpr int WS = W ? 2 * kWarps * 32 * kHMax : 0;   // double-buffered weight rows
     __shared__ __align__(16) int2 s_pair[kWarps][32];
@@ -221,9 +228,13 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     Vec<VEC> acc[CPL], cmp[CPL], tile[NT][CPL];
 #pragma unroll
     for (int q = 0; q < CPL; q++) {
-        vzero(acc[q]); vzero(cmp[q]);
+        vzero(cmp[q]);
 #pragma unroll
-        for (int k = 0; k < NT; k++) vzero(tile[k][q]);
+        for (int t = 0; t < VEC; t++) {
+            acc[q].v[t] = ID;
+#pragma unroll
+            for (int k = 0; k < NT; k++) tile[k][q].v[t] = ID;
+        }
     }
     int ntile = 0;
 
@@ -321,7 +332,8 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
                                     reinterpret_cast<const float *>(xl[q] + (uint64_t)(uint32_t)cc[k] * ldxb),
                                     pol.keep);
                         } else {
-                            vzero(x[u + k][q]);
+#pragma unroll
+                            for (int t = 0; t < VEC; t++) x[u + k][q].v[t] = ID;   // identity of the reduction
                         }
                         if constexpr (W) wt[u + k][q] = gw[(i + u + k) * H + hq[q]];
                         else wt[u + k][q] = ww[k];
@@ -334,7 +346,8 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
                 for (int q = 0; q < CPL; q++)
 #pragma unroll
                     for (int t = 0; t < VEC; t++)
-                        tile[u % NT][q].v[t] = fmaf(wt[u][q], x[u][q].v[t], tile[u % NT][q].v[t]);
+                        if constexpr (MM) tile[u % NT][q].v[t] = comb(tile[u % NT][q].v[t], x[u][q].v[t]);
+                        else tile[u % NT][q].v[t] = fmaf(wt[u][q], x[u][q].v[t], tile[u % NT][q].v[t]);
         };
         if (n == 32) {
 #pragma unroll 1
@@ -357,14 +370,20 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
             for (int q = 0; q < CPL; q++)
 #pragma unroll
                 for (int t = 0; t < VEC; t++) {
-                    float y = tile[0][q].v[t];
-                    if constexpr (NT == 2) y += tile[1][q].v[t];
-                    y -= cmp[q].v[t];
-                    const float sum = acc[q].v[t] + y;
-                    cmp[q].v[t] = (sum - acc[q].v[t]) - y;
-                    acc[q].v[t] = sum;
+                    if constexpr (MM) {
+                        float y = tile[0][q].v[t];
+                        if constexpr (NT == 2) y = comb(y, tile[1][q].v[t]);
+                        acc[q].v[t] = comb(acc[q].v[t], y);
+                    } else {
+                        float y = tile[0][q].v[t];
+                        if constexpr (NT == 2) y += tile[1][q].v[t];
+                        y -= cmp[q].v[t];
+                        const float sum = acc[q].v[t] + y;
+                        cmp[q].v[t] = (sum - acc[q].v[t]) - y;
+                        acc[q].v[t] = sum;
+                    }
 #pragma unroll
-                    for (int k = 0; k < NT; k++) tile[k][q].v[t] = 0.f;
+                    for (int k = 0; k < NT; k++) tile[k][q].v[t] = ID;
                 }
         }
     }
@@ -376,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
         for (int t = 0; t < VEC; t++) {
             float v = acc[q].v[t] - cmp[q].v[t];
 #pragma unroll
-            for (int o = LPE; o < 32; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
+            for (int o = LPE; o < 32; o <<= 1) v = comb(v, __shfl_xor_sync(kFull, v, o));
             acc[q].v[t] = v;
         }
 
@@ -392,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
                 if (f < a.F) {
                     Vec<VEC> r;
 #pragma unroll
-                    for (int t = 0; t < VEC; t++) r.v[t] = rs * acc[q].v[t];
+                    for (int t = 0; t < VEC; t++) r.v[t] = (MM && b == e) ? 0.f : rs * acc[q].v[t];   // empty row -> 0
                     vstore(a.out + row * a.ldo + f, r, a.F - f);
                 }
             }
@@ -413,9 +432,9 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     for (int t = threadIdx.x; t < SW; t += kThreads) {
         const int64_t f = f0 + t;
         if (f < a.F) {
-            float v = 0.f;
+            float v = ID;
 #pragma unroll
-            for (int w = 0; w < kWarps; w++) v += red[w * SW + t];
+            for (int w = 0; w < kWarps; w++) v = comb(v, red[w * SW + t]);
             a.out[row * a.ldo + f] = rs * v;
         }
     }
@@ -927,6 +946,64 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
     }
 }
 
+// ========================================================= NEXT-3 kernels
+// gSpMMe / gSpMMeid: out[r,h] = RED over the row's edges of w[eid, h] (sum in
+// fp64: few values per edge, any row length).  One warp per row; H | 32 maps
+// lane -> (edge offset lane / H, head lane % H), else lanes loop over heads.
+__global__ void __launch_bounds__(kThreads) spmm_e_kernel(const SpmmEArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t idx = (int64_t)blockIdx.x * kWarps + warp;
+    if (idx >= a.nrows) return;
+    const int64_t row = a.order[idx], b = a.off[row], e = a.off[row + 1];
+    const int H = (int)a.H;
+    auto red = [&](double x, double y) {
+        return a.red == 1 ? (y < x ? y : x) : (a.red == 2 ? (y > x ? y : x) : x + y);
+    };
+    const double id = a.red == 1 ? INFINITY : (a.red == 2 ? -INFINITY : 0.0);
+    if (H <= 32 && (32 % H) == 0) {
+        const int eo = lane / H, h = lane % H, step = 32 / H;
+        double acc = id;
+        for (int64_t j = b + eo; j < e; j += step) {
+            const int64_t ei = a.eid ? (int64_t)__ldg(a.eid + j) : j;
+            acc = red(acc, (double)__ldg(a.w + ei * a.ldw + h));
+        }
+        for (int o = H; o < 32; o <<= 1) acc = red(acc, __shfl_xor_sync(kFull, acc, o));
+        if (eo == 0) a.out[row * a.ldo + h] = b == e ? 0.f : (float)acc;
+    } else {
+        for (int h = lane; h < H; h += 32) {
+            double acc = id;
+            for (int64_t j = b; j < e; j++) {
+                const int64_t ei = a.eid ? (int64_t)__ldg(a.eid + j) : j;
+                acc = red(acc, (double)__ldg(a.w + ei * a.ldw + h));
+            }
+            a.out[row * a.ldo + h] = b == e ? 0.f : (float)acc;
+        }
+    }
+}
+
+// gSDDMMve: out[j,h] = w[j,h] OP X[side ? col_j : row_base + row, h]; out may be w (in place).
+__global__ void __launch_bounds__(kThreads) sddmm_ve_kernel(const SddmmVeArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t idx = (int64_t)blockIdx.x * kWarps + warp;
+    if (idx >= a.nrows) return;
+    const int64_t row = a.order[idx], b = a.off[row], e = a.off[row + 1];
+    const int64_t H = a.H;
+    const int64_t tot = (e - b) * H;
+    for (int64_t t = lane; t < tot; t += 32) {
+        const int64_t j = b + t / H, h = t % H;
+        const int64_t vx = a.side_src ? (int64_t)__ldg(a.col + j) : a.row_base + row;
+        const float x = __ldg(a.X + vx * a.ldx + h), wv = a.w[j * a.ldw + h];
+        float r;
+        switch (a.op) {
+            case 0: r = wv + x; break;
+            case 1: r = wv - x; break;
+            case 2: r = wv * x; break;
+            default: r = wv / x; break;
+        }
+        a.out[j * a.ldo + h] = r;
+    }
+}
+
 // ==================================================== edge softmax backward
 // ds[j,h] = alpha[j,h] * (dalpha[j,h] - <alpha[row,h], dalpha[row,h]>)   (NEXT-1)
 // Fast path: contiguous [E, H], H % 4 == 0, H | 32 (lane owns heads (4 lane + t) mod H).
@@ -1035,8 +1112,12 @@ cudaError_t spmm_go_v(const SpmmArgs &a, int mode, int64_t slabs, cudaStream_t s
         else spmm_kernel<VEC, LPE, CPL, kSpmmScaled, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
     } else if (mode == kSpmmWeightedFwd) {
         spmm_kernel<VEC, LPE, CPL, kSpmmWeightedFwd, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
-    } else {
+    } else if (mode == kSpmmWeightedRev) {
         spmm_kernel<VEC, LPE, CPL, kSpmmWeightedRev, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
+    } else if (mode == kSpmmMin) {
+        spmm_kernel<VEC, LPE, CPL, kSpmmMin, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
+    } else {
+        spmm_kernel<VEC, LPE, CPL, kSpmmMax, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
     }
     return cudaGetLastError();
 }
@@ -1154,7 +1235,7 @@ cudaError_t sddmm_dispatch(const SddmmArgs &a, int cph, cudaStream_t s) {
 
 cudaError_t launch_spmm(const SpmmArgs &a, int mode, cudaStream_t s) {
     if (a.nrows == 0 || a.F == 0) return cudaSuccess;
-    const bool wmode = mode != kSpmmScaled;
+    const bool wmode = mode == kSpmmWeightedFwd || mode == kSpmmWeightedRev;
     if (wmode && a.H > kHMax) return cudaErrorNotSupported;   // api.cu rejects H > 16 first
     auto ok_vec = [&](int v) {
         return a.F >= v && a.ldx % v == 0 && a.ldo % 4 == 0 && aligned(a.X, 4 * v) && aligned(a.out, 16) &&
@@ -1236,6 +1317,18 @@ cudaError_t launch_gat_fused(const GatArgs &a, cudaStream_t s) {
             else gat_fused_kernel<32, false><<<grid, kThreads, 0, s>>>(a);
     }
 #undef GSP_GAT_CASE
+    return cudaGetLastError();
+}
+
+cudaError_t launch_spmm_e(const SpmmEArgs &a, cudaStream_t s) {
+    if (a.nrows == 0 || a.H == 0) return cudaSuccess;
+    spmm_e_kernel<<<(unsigned)ceil_div(a.nrows, kWarps), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sddmm_ve(const SddmmVeArgs &a, cudaStream_t s) {
+    if (a.nrows == 0 || a.H == 0) return cudaSuccess;
+    sddmm_ve_kernel<<<(unsigned)ceil_div(a.nrows, kWarps), kThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -25,7 +25,7 @@ struct SpmmArgs {
     int64_t H, Fh;
 };
 
-enum SpmmMode { kSpmmScaled = 0, kSpmmWeightedFwd = 1, kSpmmWeightedRev = 2 };
+enum SpmmMode { kSpmmScaled = 0, kSpmmWeightedFwd = 1, kSpmmWeightedRev = 2, kSpmmMin = 3, kSpmmMax = 4 };
 
 cudaError_t launch_spmm(const SpmmArgs &a, int mode, cudaStream_t s);
 
@@ -93,6 +93,38 @@ struct GatArgs {
 };
 bool gat_fused_supported(const GatArgs &a);
 cudaError_t launch_gat_fused(const GatArgs &a, cudaStream_t s);
+
+// NEXT-3 (Table 1 surface): gSpMMe / gSpMMeid and gSDDMMve.
+struct SpmmEArgs {
+    const int64_t *off;
+    const int32_t *eid;      // null: implicit (slot = edge id)
+    const int32_t *order;
+    int64_t nrows;
+    const float *w;
+    int64_t ldw;
+    float *out;
+    int64_t ldo;
+    int64_t H;
+    int red;                 // 0 sum, 1 min, 2 max
+};
+cudaError_t launch_spmm_e(const SpmmEArgs &a, cudaStream_t s);
+
+struct SddmmVeArgs {
+    const int64_t *off;
+    const int32_t *col;
+    const int32_t *order;
+    int64_t nrows, row_base;
+    const float *X;
+    int64_t ldx;
+    const float *w;
+    int64_t ldw;
+    float *out;
+    int64_t ldo;
+    int64_t H;
+    int op;                  // 0 add, 1 sub, 2 mul, 3 div
+    int side_src;            // 1: X indexed by the column (source), 0: by the row (destination)
+};
+cudaError_t launch_sddmm_ve(const SddmmVeArgs &a, cudaStream_t s);
 
 // fp32 degree scales from (clamped) integer degrees: inv = 1/d^, rsq = d^^-1/2
 // computed in fp64 then rounded once.

@@ -18,6 +18,9 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_PKG, "libgsp.so")
 
 NORM_NONE, NORM_RIGHT, NORM_BOTH = 0, 1, 2
+REDUCE_SUM, REDUCE_MIN, REDUCE_MAX = 0, 1, 2
+OP_ADD, OP_SUB, OP_MUL, OP_DIV = 0, 1, 2, 3
+SIDE_DST, SIDE_SRC = 0, 1
 BUILD_REVERSE, BUILD_SHARE_SYMMETRIC = 1, 2
 PART_REVERSE = 1
 
@@ -27,7 +30,7 @@ STATUS = {0: "GSP_OK", 1: "GSP_ERR_NULL", 2: "GSP_ERR_ARG", 3: "GSP_ERR_VERTEX_R
 # the exported C symbols (include/gsp.h), checked by tests/test_abi.py
 SYMBOLS = ["gsp_graph_create", "gsp_graph_destroy", "gsp_graph_info", "gsp_graph_export", "gsp_gspmm",
            "gsp_gspmm_weighted", "gsp_gsddmm", "gsp_edge_softmax", "gsp_edge_softmax_backward",
-           "gsp_gat_forward", "gsp_partition_bounds", "gsp_graph_partition",
+           "gsp_gat_forward", "gsp_gspmm_reduce", "gsp_gspmm_e", "gsp_gsddmm_ve", "gsp_partition_bounds", "gsp_graph_partition",
            "gsp_partition_info", "gsp_status_string", "gsp_last_error_detail", "gsp_version"]
 
 
@@ -62,6 +65,9 @@ def _load():
         "gsp_edge_softmax": ([p, T, T, p], ci),
         "gsp_edge_softmax_backward": ([p, T, T, T, p], ci),
         "gsp_gat_forward": ([p, T, T, T, T, T, p], ci),
+        "gsp_gspmm_reduce": ([p, T, ci, T, ci, p], ci),
+        "gsp_gspmm_e": ([p, T, ci, T, ci, p], ci),
+        "gsp_gsddmm_ve": ([p, T, T, ci, ci, T, p], ci),
         "gsp_partition_bounds": ([p, ci, ci, p], ci),
         "gsp_graph_partition": ([p, ci, ci, ci, u32, P(p)], ci),
         "gsp_partition_info": ([p, P(ci), P(ci), P(i64), P(i64), P(i64), P(i64), P(ci)], ci),
@@ -237,6 +243,38 @@ def _gat_forward(self, X, Y, Vt, H, alpha=None, out=None, stream=None):
 
 
 Graph.gat_forward = _gat_forward
+
+
+def _gspmm_reduce(self, X, reduce, out=None, reverse=False, stream=None):
+    if out is None:
+        out = self._alloc(self.V, X.shape[1], X)
+    dx, do = _desc(X), _desc(out)
+    _check(lib.gsp_gspmm_reduce(self._h, ctypes.byref(dx), int(reduce), ctypes.byref(do), int(bool(reverse)),
+                                _stream(stream, X.device)))
+    return out
+
+
+def _gspmm_e(self, w, reduce, out=None, reverse=False, stream=None):
+    if out is None:
+        out = self._alloc(self.ncols if reverse else self.V, w.shape[1], w)
+    dw, do = _desc(w), _desc(out)
+    _check(lib.gsp_gspmm_e(self._h, ctypes.byref(dw), int(reduce), ctypes.byref(do), int(bool(reverse)),
+                           _stream(stream, w.device)))
+    return out
+
+
+def _gsddmm_ve(self, X, w, op, side, out=None, stream=None):
+    if out is None:
+        out = self._alloc(self.E, w.shape[1], w)
+    dx, dw, do = _desc(X), _desc(w), _desc(out)
+    _check(lib.gsp_gsddmm_ve(self._h, ctypes.byref(dx), ctypes.byref(dw), int(op), int(side), ctypes.byref(do),
+                             _stream(stream, w.device)))
+    return out
+
+
+Graph.gspmm_reduce = _gspmm_reduce
+Graph.gspmm_e = _gspmm_e
+Graph.gsddmm_ve = _gsddmm_ve
 
 
 def version():

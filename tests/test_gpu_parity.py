@@ -445,3 +445,69 @@ def test_gat_forward_heavy_rows_and_pubmed(gsp):
     cfg = datagen.CONFIGS["pubmed"]
     V, src, dst = datagen.make_graph(cfg)
     _gat_check(gsp, V, src, dst, 8, 8, 8, True, seed=4)
+
+
+# ------------------------------------------- NEXT-3: Table 1 surface (min/max, gSpMMe, gSDDMMve)
+@pytest.mark.parametrize("F,ld", [(1, 1), (5, 8), (16, 16), (64, 64), (100, 100), (602, 604)])
+def test_gspmm_reduce_minmax(gsp, F, ld):
+    for seed in range(2):
+        rng = np.random.default_rng(seed + F)
+        V = int(rng.integers(1, 2500))
+        E = int(rng.integers(0, 30000))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed == 0
+                    else datagen.skewed_multigraph(V, E, seed, alpha=1.6))
+        G, og = graph_pair(gsp, V, src, dst)
+        Xh = datagen.uniform(seed + 3, V, F)
+        X = padded(Xh, ld)
+        for red in (gsp.REDUCE_MIN, gsp.REDUCE_MAX, gsp.REDUCE_SUM):
+            for rev in (0, 1):
+                ref, T = og.gspmm_reduce(Xh, red, bool(rev))
+                out = G.gspmm_reduce(X, red, reverse=rev).cpu().numpy()
+                if red == gsp.REDUCE_SUM:
+                    assert_within(out, ref, T, f"sum r{rev}")
+                else:   # min / max pick an input exactly
+                    assert np.array_equal(out.astype(np.float64), ref), (red, rev)
+
+
+@pytest.mark.parametrize("H", [1, 2, 8, 5, 40])
+def test_gspmm_e(gsp, H):
+    for seed in range(2):
+        rng = np.random.default_rng(seed + 3 * H)
+        V = int(rng.integers(1, 2500))
+        E = int(rng.integers(0, 30000))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed == 0
+                    else datagen.skewed_multigraph(V, E, seed, alpha=1.6))
+        G, og = graph_pair(gsp, V, src, dst)
+        wh = datagen.uniform(seed + 5, E, H) if E else np.zeros((0, H), np.float32)
+        for red in (gsp.REDUCE_SUM, gsp.REDUCE_MIN, gsp.REDUCE_MAX):
+            for rev in (0, 1):
+                ref, T = og.gspmm_e(wh, red, bool(rev))
+                out = G.gspmm_e(dev(wh), red, reverse=rev).cpu().numpy()
+                if red == gsp.REDUCE_SUM:
+                    assert_within(out, ref, T, f"gspmm_e sum r{rev}")
+                else:
+                    assert np.array_equal(out.astype(np.float64), ref), (red, rev)
+
+
+@pytest.mark.parametrize("H", [1, 3, 8])
+def test_gsddmm_ve(gsp, H):
+    rng = np.random.default_rng(H)
+    V = int(rng.integers(1, 2500))
+    E = int(rng.integers(1, 30000))
+    src, dst = datagen.skewed_multigraph(V, E, H, alpha=1.5)
+    G, og = graph_pair(gsp, V, src, dst)
+    Xh = datagen.uniform(1, V, H, lo=0.5, hi=2.0)
+    wh = datagen.uniform(2, E, H)
+    for op in (gsp.OP_ADD, gsp.OP_SUB, gsp.OP_MUL, gsp.OP_DIV):
+        for side in (gsp.SIDE_DST, gsp.SIDE_SRC):
+            ref = og.gsddmm_ve(Xh, wh, op, side)
+            out = G.gsddmm_ve(dev(Xh), dev(wh), op, side).cpu().numpy()
+            # one IEEE fp32 operation on exact fp32 inputs: correctly rounded
+            assert np.array_equal(out, ref.astype(np.float32)), (op, side)
+    # additive GAT scores: e = a_dst[v] + a_src[u] as two calls, the second in place
+    a_dst, a_src = datagen.uniform(3, V, H), datagen.uniform(4, V, H)
+    e = G.gsddmm_ve(dev(a_dst), torch.zeros((E, H), device="cuda"), gsp.OP_ADD, gsp.SIDE_DST)
+    G.gsddmm_ve(dev(a_src), e, gsp.OP_ADD, gsp.SIDE_SRC, out=e)
+    row_of = np.repeat(np.arange(V), np.diff(og.fwd_off))
+    ref = (a_dst[row_of].astype(np.float32) + a_src[og.fwd_col].astype(np.float32))
+    assert np.array_equal(e.cpu().numpy(), ref)

@@ -505,3 +505,81 @@ def test_gat_forward_is_the_composition(seed):
     np.add.at(sums, rows, a)
     nz = np.diff(G.fwd_off) > 0
     assert np.allclose(sums[nz], 1.0, atol=1e-13)
+
+
+# ----------------------------------------------- C11-C13 Table-1 surface (NEXT-3)
+def coo_reduce(V, keys, vals, red):
+    """Brute force: reduce vals grouped by keys (COO order, no CSR), empty -> 0."""
+    F = vals.shape[1]
+    out = np.zeros((V, F))
+    for v in range(V):
+        m = keys == v
+        if m.any():
+            blk = vals[m].astype(np.float64)
+            out[v] = blk.sum(0) if red == oracle.RED_SUM else (blk.min(0) if red == oracle.RED_MIN else blk.max(0))
+    return out
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_gspmm_reduce_bruteforce(seed):
+    V, src, dst = rand_graph(10000 + seed)
+    G = oracle.Graph(V, src, dst)
+    X = datagen.uniform(seed, V, 3)
+    for red in (oracle.RED_SUM, oracle.RED_MIN, oracle.RED_MAX):
+        out, T = G.gspmm_reduce(X, red, False)
+        assert np.allclose(out, coo_reduce(V, dst, X[src], red), atol=1e-12)
+        out, T = G.gspmm_reduce(X, red, True)
+        assert np.allclose(out, coo_reduce(V, src, X[dst], red), atol=1e-12)
+    s, _ = G.gspmm_reduce(X, oracle.RED_SUM)
+    assert np.allclose(s, G.gspmm(X, NORM_NONE)[0], atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_gspmm_e_bruteforce(seed):
+    V, src, dst = rand_graph(11000 + seed)
+    G = oracle.Graph(V, src, dst)
+    H = 1 + seed % 3
+    w_coo = datagen.uniform(seed, G.E, H) if G.E else np.zeros((0, H), np.float32)
+    w = np.zeros_like(w_coo)
+    w[G.coo_to_eid] = w_coo
+    for red in (oracle.RED_SUM, oracle.RED_MIN, oracle.RED_MAX):
+        assert np.allclose(G.gspmm_e(w, red, False)[0], coo_reduce(V, dst, w_coo, red), atol=1e-12)
+        assert np.allclose(G.gspmm_e(w, red, True)[0], coo_reduce(V, src, w_coo, red), atol=1e-12)
+
+
+def test_gspmm_e_spec_examples(golden):
+    g = golden("t4.json")
+    G = oracle.Graph(g["V"], g["src"], g["dst"])
+    # SPEC S:187-189: all-ones sum -> degrees; max over T4 row 2 with We[j] = j -> 6
+    assert G.gspmm_e(np.ones((8, 1), np.float32), oracle.RED_SUM)[0][:, 0].tolist() == g["deg"]
+    assert G.gspmm_e(np.arange(8, dtype=np.float32)[:, None], oracle.RED_MAX)[0][2, 0] == 6.0
+    G5 = oracle.Graph(5, g["src"], g["dst"])
+    for red in (oracle.RED_SUM, oracle.RED_MIN, oracle.RED_MAX):   # empty row -> 0 (SPEC S:237)
+        assert G5.gspmm_e(np.ones((8, 1), np.float32), red)[0][4, 0] == 0.0
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_gsddmm_ve_bruteforce(seed):
+    V, src, dst = rand_graph(12000 + seed)
+    G = oracle.Graph(V, src, dst)
+    H = 1 + seed % 3
+    X = datagen.uniform(seed, V, H, lo=0.5, hi=2.0)
+    w = datagen.uniform(seed + 1, G.E, H) if G.E else np.zeros((0, H), np.float32)
+    row_of = np.repeat(np.arange(V), np.diff(G.fwd_off))
+    for op, f in [(oracle.OP_ADD, np.add), (oracle.OP_SUB, np.subtract), (oracle.OP_MUL, np.multiply),
+                  (oracle.OP_DIV, np.divide)]:
+        for side in (0, 1):
+            vx = G.fwd_col if side else row_of
+            ref = f(w.astype(np.float64), X[vx].astype(np.float64))
+            assert np.allclose(G.gsddmm_ve(X, w, op, side), ref, atol=1e-12)
+
+
+def test_gsddmm_ve_spec_examples(golden):
+    g = golden("t4.json")
+    G = oracle.Graph(g["V"], g["src"], g["dst"])
+    w = datagen.uniform(1, 8, 1)
+    # SPEC S:204-206: sub of zeros -> w; mul of ones on the column side -> gather X[col]
+    assert np.array_equal(G.gsddmm_ve(np.zeros((4, 1), np.float32), w, oracle.OP_SUB, 0), w.astype(np.float64))
+    X = np.array(g["X"], np.float32)[:, None]
+    out = G.gsddmm_ve(X, np.ones((8, 1), np.float32), oracle.OP_MUL, 1)
+    assert out[:, 0].tolist() == [X[c, 0] for c in g["fwd_col"]]
