@@ -25,7 +25,7 @@ def build(force: bool = False) -> str:
     """Compile gen.c into libgspgen.so (gcc, -O2)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
         tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-std=c11", "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-std=c11", "-fopenmp", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _SO)
     return _SO
 
@@ -43,6 +43,8 @@ def _L():
         lib.gen_chung_lu.restype = ctypes.c_int
         lib.gen_rmat.argtypes = [ctypes.c_int, i64, i64, dbl, dbl, dbl, u64, p64, p64]
         lib.gen_rmat.restype = ctypes.c_int
+        lib.gen_kron.argtypes = [ctypes.c_int, i64, dbl, dbl, dbl, u64, p64, p64]
+        lib.gen_kron.restype = ctypes.c_int
         lib.gen_uniform_f32.argtypes = [u64, i64, i64, i64, ctypes.c_float, ctypes.c_float, p64]
         lib.gen_uniform_f32.restype = None
         _lib = lib
@@ -66,6 +68,17 @@ def rmat(scale: int, V: int, E: int, seed: int, a=0.57, b=0.19, c=0.19):
     rc = _L().gen_rmat(scale, V, E, a, b, c, seed, src.ctypes.data, dst.ctypes.data)
     if rc != 0:
         raise RuntimeError(f"gen_rmat failed rc={rc}")
+    return src, dst
+
+
+def kron(scale: int, npairs: int, seed: int, a=0.57, b=0.19, c=0.19):
+    """Graph500-style Kronecker graph: 2*npairs directed edges (duplicates and
+    self-loops kept), 2^scale vertices, seeded relabelling."""
+    src = np.empty(2 * npairs, dtype=np.int64)
+    dst = np.empty(2 * npairs, dtype=np.int64)
+    rc = _L().gen_kron(scale, npairs, a, b, c, seed, src.ctypes.data, dst.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(f"gen_kron failed rc={rc}")
     return src, dst
 
 
@@ -143,6 +156,9 @@ CONFIGS = {
     "arxiv": GraphConfig("arxiv", "rmat", 169343, 1166243, scale=18, seed=0xA5C1, F=128, ld=128),
     "reddit": GraphConfig("reddit", "chung_lu", 232965, 114615892, beta=0.3398, seed=0x2EDD, F=64, ld=64, H=8, Fh=8),
     "products": GraphConfig("products", "chung_lu", 2449029, 123718280, beta=0.4364, seed=0x960D, F=100, ld=100),
+    # the paper's billion-edge Kron-25 (Table 2): Graph500 Kronecker,
+    # 2^25 vertices, 2^29 draws emitted in both directions = 2^30 edges, F = 150 (ld 152)
+    "kron25": GraphConfig("kron25", "kron", 1 << 25, 1 << 30, scale=25, seed=0xC125, F=150, ld=152),
 }
 
 
@@ -153,6 +169,8 @@ def make_graph(cfg: GraphConfig | str):
     if cfg.kind == "chung_lu":
         assert cfg.E % 2 == 0
         src, dst = chung_lu(cfg.V, cfg.E // 2, cfg.beta, cfg.seed)
+    elif cfg.kind == "kron":
+        src, dst = kron(cfg.scale, cfg.E // 2, cfg.seed)
     else:
         src, dst = rmat(cfg.scale, cfg.V, cfg.E, cfg.seed)
     return cfg.V, src, dst

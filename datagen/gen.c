@@ -192,12 +192,57 @@ int gen_rmat(int scale, int64_t V, int64_t E, double a, double b, double c,
     return relabel_and_shuffle(&rng, V, E, src, dst);
 }
 
+/* ----------------------------------------------------------- Kronecker --- */
+/* Graph500-style Kronecker graph (the paper's Kron-25, PAPER Table 2:
+ * 2^25 vertices, 2^30 edges): npairs R-MAT draws with quadrant probabilities
+ * (a, b, c, 1-a-b-c), duplicates and self-loops KEPT (the edge count is exact),
+ * each emitted in both directions, then a seeded vertex relabelling.  Every
+ * draw k uses a counter-based stream (seed, k, level), so the result does not
+ * depend on the number of threads. */
+int gen_kron(int scale, int64_t npairs, double a, double b, double c, uint64_t seed, int64_t *src, int64_t *dst) {
+    if (scale < 1 || scale > 40) return -2;
+    const int64_t V = (int64_t)1 << scale;
+    const double ab = a + b, abc = a + b + c;
+    const uint64_t s0 = mix64(seed ^ 0xA0761D6478BD642FULL);
+    #pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < npairs; k++) {
+        uint64_t st = mix64(s0 + (uint64_t)k * 0x9E3779B97F4A7C15ULL);
+        int64_t u = 0, v = 0;
+        for (int l = 0; l < scale; l++) {
+            st = mix64(st + 0xD1B54A32D192ED03ULL);
+            double r = (double)(st >> 11) * 0x1.0p-53;
+            int bu, bv;
+            if (r < a) { bu = 0; bv = 0; }
+            else if (r < ab) { bu = 0; bv = 1; }
+            else if (r < abc) { bu = 1; bv = 0; }
+            else { bu = 1; bv = 1; }
+            u = (u << 1) | bu; v = (v << 1) | bv;
+        }
+        src[2 * k] = u; dst[2 * k] = v;
+        src[2 * k + 1] = v; dst[2 * k + 1] = u;
+    }
+    /* seeded relabelling (Fisher-Yates), applied in parallel */
+    xo256 rng; xo_seed(&rng, seed);
+    int64_t *perm = (int64_t *)malloc(sizeof(int64_t) * (size_t)V);
+    if (!perm) return -1;
+    for (int64_t i = 0; i < V; i++) perm[i] = i;
+    for (int64_t i = V - 1; i > 0; i--) {
+        int64_t j = (int64_t)xo_below(&rng, (uint64_t)(i + 1));
+        int64_t t = perm[i]; perm[i] = perm[j]; perm[j] = t;
+    }
+    #pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < 2 * npairs; e++) { src[e] = perm[src[e]]; dst[e] = perm[dst[e]]; }
+    free(perm);
+    return 0;
+}
+
 /* ------------------------------------------------------- features -------- */
 /* Counter-based U[lo,hi) fp32 with 24 random bits per element: element (r,c)
  * depends only on (seed,r,c).  Padding columns [cols,ld) are set to 0. */
 void gen_uniform_f32(uint64_t seed, int64_t rows, int64_t cols, int64_t ld,
                      float lo, float hi, float *out) {
     const uint64_t s0 = mix64(seed ^ 0x5DEECE66DULL);
+    #pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < rows; r++) {
         const uint64_t sr = mix64(s0 + (uint64_t)r * 0x9E3779B97F4A7C15ULL);
         float *row = out + r * ld;

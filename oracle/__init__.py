@@ -68,6 +68,10 @@ def _L():
         lib.oracle_gspmm_e.restype = ci
         lib.oracle_gsddmm_ve.argtypes = [i64, p, p, p, p, i64, ci, ci, p]
         lib.oracle_gsddmm_ve.restype = ci
+        lib.oracle_gspmm_rows_coo.argtypes = [i64, i64, p, p, p, i64, i64, ci, ci, i64, p, p, p]
+        lib.oracle_gspmm_rows_coo.restype = ci
+        lib.oracle_rows_coo.argtypes = [i64, i64, p, p, i64, p, p, p, p]
+        lib.oracle_rows_coo.restype = ci
         lib.oracle_partition_bounds.argtypes = [i64, p, i64, p]
         lib.oracle_partition_bounds.restype = ci
         lib.oracle_partition_structure.argtypes = [i64, p, p, i64, p, i64, p, p]
@@ -280,3 +284,36 @@ class Graph:
 def bound(T):
     """Acceptance bound of BASELINE.json: 1e-5 * (sum|terms| + 1) per element."""
     return 1e-5 * (np.asarray(T) + 1.0)
+
+
+# ------------------------------------------------ row-sampled oracle from COO
+def gspmm_rows_coo(V, src, dst, X, norm, rows, reverse=False, F=None):
+    """C4 for the selected rows straight from the COO list (no build)."""
+    src = _c(src, np.int64)
+    dst = _c(dst, np.int64)
+    X = _c(X, np.float32)
+    F = X.shape[1] if F is None else F
+    rows = _c(rows, np.int64)
+    out = np.empty((len(rows), F), np.float64)
+    T = np.empty((len(rows), F), np.float64)
+    rc = _L().oracle_gspmm_rows_coo(V, len(src), _ptr(src), _ptr(dst), _ptr(X), F, X.shape[1], norm,
+                                    int(bool(reverse)), len(rows), _ptr(rows), _ptr(out), _ptr(T))
+    assert rc == 0, rc
+    return out, T
+
+
+def rows_coo(V, src, dst, rows):
+    """C1 for the selected destination rows from the COO list: per row the
+    sorted (src, position) pairs of its in-edges and its first fwd slot."""
+    src = _c(src, np.int64)
+    dst = _c(dst, np.int64)
+    rows = _c(rows, np.int64)
+    off = np.empty(len(rows) + 1, np.int64)
+    first = np.empty(len(rows), np.int64)
+    tot = int(sum(int(np.count_nonzero(dst == v)) for v in rows)) if len(src) < (1 << 24) else \
+        int(np.bincount(dst, minlength=V)[rows].sum())
+    pairs = np.empty(2 * max(tot, 1), np.int64)
+    rc = _L().oracle_rows_coo(V, len(src), _ptr(dst), _ptr(src), len(rows), _ptr(rows), _ptr(off), _ptr(first),
+                              _ptr(pairs))
+    assert rc == 0, rc
+    return [(int(first[r]), pairs[2 * off[r]:2 * off[r + 1]].reshape(-1, 2)) for r in range(len(rows))]

@@ -395,6 +395,93 @@ int oracle_gsddmm_ve(int64_t V, const int64_t *fwd_off, const int32_t *fwd_col, 
     return 0;
 }
 
+/* ----------------------------------------------------- C4/C1 from COO --- */
+/* The same definitions evaluated straight from the COO list for a few
+ * selected rows (billion-edge graphs, where sorting the whole edge list in the
+ * oracle is impractical).  Degrees by counting; every COO edge whose
+ * destination (reverse: source) is a selected row contributes once:
+ *   fwd: out[r,f] = s_dst(v) * sum_{i: dst[i]=v} s_src(src[i]) X[src[i], f]   (C4)
+ * and the row's fwd slots are its COO edges sorted by (src, position) (C1). */
+int oracle_gspmm_rows_coo(int64_t V, int64_t E, const int64_t *src, const int64_t *dst, const float *X, int64_t F,
+                          int64_t ldx, int norm, int reverse, int64_t nsel, const int64_t *sel, double *out,
+                          double *T) {
+    int64_t *din = (int64_t *)calloc((size_t)V, sizeof(int64_t)), *dout = (int64_t *)calloc((size_t)V, sizeof(int64_t));
+    int32_t *slot = (int32_t *)malloc(sizeof(int32_t) * (size_t)V);
+    if (!din || !dout || !slot) { free(din); free(dout); free(slot); return -2; }
+    for (int64_t i = 0; i < E; i++) { din[dst[i]]++; dout[src[i]]++; }
+    for (int64_t v = 0; v < V; v++) slot[v] = -1;
+    for (int64_t r = 0; r < nsel; r++) slot[sel[r]] = (int32_t)r;
+    for (int64_t r = 0; r < nsel * F; r++) { out[r] = 0.0; if (T) T[r] = 0.0; }
+    for (int64_t i = 0; i < E; i++) {
+        int64_t row = reverse ? src[i] : dst[i], c = reverse ? dst[i] : src[i];
+        int32_t r = slot[row];
+        if (r < 0) continue;
+        /* column-side scale: fwd -> s_src(c) from d_out; rev -> s_dst(c) from d_in */
+        double dc = (double)(reverse ? din[c] : dout[c]);
+        if (dc < 1.0) dc = 1.0;
+        double cs = 1.0;
+        if (norm == OR_NORM_BOTH) cs = 1.0 / sqrt(dc);
+        else if (norm == OR_NORM_RIGHT && reverse) cs = 1.0 / dc;
+        for (int64_t f = 0; f < F; f++) {
+            double t = cs * (double)X[c * ldx + f];
+            out[r * F + f] += t;
+            if (T) T[r * F + f] += fabs(t);
+        }
+    }
+    for (int64_t r = 0; r < nsel; r++) {
+        int64_t v = sel[r];
+        double dr = (double)(reverse ? dout[v] : din[v]);
+        if (dr < 1.0) dr = 1.0;
+        double rs = 1.0;
+        if (norm == OR_NORM_BOTH) rs = 1.0 / sqrt(dr);
+        else if (norm == OR_NORM_RIGHT && !reverse) rs = 1.0 / dr;
+        for (int64_t f = 0; f < F; f++) { out[r * F + f] *= rs; if (T) T[r * F + f] *= rs; }
+    }
+    free(din); free(dout); free(slot);
+    return 0;
+}
+
+/* For each selected destination row, its in-edges from the COO list as
+ * (src, position) pairs sorted by (src, position) = the row's fwd slots (C1),
+ * plus fwd_off[v] = #{i : dst[i] < v}.  pairs has room for the rows' degrees. */
+static int cmp_pair(const void *a, const void *b) {
+    const int64_t *x = (const int64_t *)a, *y = (const int64_t *)b;
+    if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;
+    return x[1] < y[1] ? -1 : (x[1] > y[1]);
+}
+int oracle_rows_coo(int64_t V, int64_t E, const int64_t *dst_, const int64_t *src_, int64_t nsel, const int64_t *sel,
+                    int64_t *row_off /* nsel+1, prefix of degrees */, int64_t *first_slot /* nsel */,
+                    int64_t *pairs /* 2 * sum deg */) {
+    int32_t *slot = (int32_t *)malloc(sizeof(int32_t) * (size_t)V);
+    int64_t *cnt = (int64_t *)calloc((size_t)nsel, sizeof(int64_t));
+    int64_t *hist = (int64_t *)calloc((size_t)V + 1, sizeof(int64_t));
+    if (!slot || !cnt || !hist) { free(slot); free(cnt); free(hist); return -2; }
+    for (int64_t v = 0; v < V; v++) slot[v] = -1;
+    for (int64_t r = 0; r < nsel; r++) slot[sel[r]] = (int32_t)r;
+    for (int64_t i = 0; i < E; i++) {
+        hist[dst_[i] + 1]++;                      /* fwd_off[v] = #{i : dst[i] < v} */
+        int32_t r = slot[dst_[i]];
+        if (r >= 0) cnt[r]++;
+    }
+    for (int64_t v = 0; v < V; v++) hist[v + 1] += hist[v];
+    for (int64_t r = 0; r < nsel; r++) first_slot[r] = hist[sel[r]];
+    free(hist);
+    row_off[0] = 0;
+    for (int64_t r = 0; r < nsel; r++) row_off[r + 1] = row_off[r] + cnt[r];
+    for (int64_t r = 0; r < nsel; r++) cnt[r] = 0;
+    for (int64_t i = 0; i < E; i++) {
+        int32_t r = slot[dst_[i]];
+        if (r < 0) continue;
+        int64_t k = row_off[r] + cnt[r]++;
+        pairs[2 * k] = src_[i];
+        pairs[2 * k + 1] = i;
+    }
+    for (int64_t r = 0; r < nsel; r++)
+        qsort(pairs + 2 * row_off[r], (size_t)(row_off[r + 1] - row_off[r]), 2 * sizeof(int64_t), cmp_pair);
+    free(slot); free(cnt);
+    return 0;
+}
+
 /* ------------------------------------------------------------------ C8 --- */
 /* Edge-balanced contiguous row partition (BJ north_star
  * "destination-row partitioner"):  b_0 = 0, b_P = V,

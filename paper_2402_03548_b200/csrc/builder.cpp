@@ -21,8 +21,8 @@ int pick_threads(int64_t n, int64_t nkeys) {
     unsigned hc = std::thread::hardware_concurrency();
     int t = (int)std::min<unsigned>(hc ? hc : 1, 16);
     if (n < (1 << 16)) t = 1;
-    // keep the per-thread histograms (t * nkeys * 4 B) under ~512 MB
-    while (t > 1 && (double)t * (double)nkeys * 4.0 > 512e6) t--;
+    // keep the per-thread histograms (t * nkeys * 4 B) under ~2 GB
+    while (t > 1 && (double)t * (double)nkeys * 4.0 > 2e9) t--;
     return std::max(t, 1);
 }
 

@@ -111,3 +111,32 @@ def test_products_gspmm_sampled():
     out = G.gspmm(dev(Xh), 2).cpu().numpy()
     ref, T = og.gspmm(Xh, 2, False, rows=rows)
     within(out[rows], ref, T)
+
+
+def test_kron25_billion_edges():
+    """NEXT-4: the paper's billion-edge Kron-25 (2^25 vertices, 2^30 edges,
+    F = 150) built and aggregated on ONE B200.  Structure of
+    sampled rows bit-exact and GCN gSpMM (BOTH) on sampled rows within the
+    bound, both against the oracle evaluated straight from the COO list."""
+    import paper_2402_03548_b200 as gsp
+    cfg = datagen.CONFIGS["kron25"]
+    V, src, dst = datagen.make_graph(cfg)
+    G = gsp.Graph(V, src, dst, device=0)
+    assert G.E == 1 << 30 and G.symmetric
+    ex = G.export(rev=False, coo=False)
+    deg = np.diff(ex["fwd_off"])
+    order = np.argsort(-deg, kind="stable")
+    rng = np.random.default_rng(25)
+    rows = np.unique(np.concatenate([order[:6], rng.choice(V, 20, replace=False), order[-4:]])).astype(np.int64)
+    for (first, pairs), v in zip(oracle.rows_coo(V, src, dst, rows), rows):
+        assert first == ex["fwd_off"][v]
+        assert np.array_equal(pairs[:, 0], ex["fwd_col"][ex["fwd_off"][v]:ex["fwd_off"][v + 1]])
+    del ex
+    Xh = datagen.uniform(0xC125, V, cfg.F, ld=cfg.ld)
+    X = torch.from_numpy(Xh).cuda()[:, :cfg.F]
+    out = G.gspmm(X, gsp.NORM_BOTH)
+    torch.cuda.synchronize()
+    got = out[torch.from_numpy(rows).cuda()].cpu().numpy()
+    del out, X
+    ref, T = oracle.gspmm_rows_coo(V, src, dst, Xh, 2, rows, F=cfg.F)
+    within(got, ref, T)

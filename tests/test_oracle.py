@@ -583,3 +583,23 @@ def test_gsddmm_ve_spec_examples(golden):
     X = np.array(g["X"], np.float32)[:, None]
     out = G.gsddmm_ve(X, np.ones((8, 1), np.float32), oracle.OP_MUL, 1)
     assert out[:, 0].tolist() == [X[c, 0] for c in g["fwd_col"]]
+
+
+# ------------------------------------------- row-sampled COO oracle (NEXT-4)
+@pytest.mark.parametrize("seed", range(10))
+def test_rows_coo_matches_full_oracle(seed):
+    """The COO-scan evaluation of C4 / C1 for selected rows equals the full
+    oracle (itself pinned above) on the same graph."""
+    V, src, dst = rand_graph(13000 + seed, Vmax=80, Emax=600)
+    G = oracle.Graph(V, src, dst)
+    X = datagen.uniform(seed, V, 4)
+    rows = np.unique(np.random.default_rng(seed).integers(0, V, size=min(V, 9)))
+    for norm in (NORM_NONE, NORM_RIGHT, NORM_BOTH):
+        for rev in (False, True):
+            ref, T = G.gspmm(X, norm, rev, rows=rows)
+            out, T2 = oracle.gspmm_rows_coo(V, src, dst, X, norm, rows, rev)
+            assert np.allclose(out, ref, atol=1e-12) and np.allclose(T, T2, atol=1e-12)
+    for (first, pairs), v in zip(oracle.rows_coo(V, src, dst, rows), rows):
+        assert first == G.fwd_off[v]
+        assert np.array_equal(pairs[:, 0], G.fwd_col[G.fwd_off[v]:G.fwd_off[v + 1]])
+        assert np.array_equal(G.coo_to_eid[pairs[:, 1]], np.arange(G.fwd_off[v], G.fwd_off[v + 1]))
