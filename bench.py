@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e / cpu baseline / clocks)")
+    ap.add_argument("--check", action="store_true", help="N > 1: compare the exchanged outputs with the full graph")
     return ap.parse_args()
 
 
@@ -202,9 +203,16 @@ def main_gsp(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # one process per GPU; GSP_BENCH_BACKEND=gloo lets a 1-GPU box run N ranks on one device
+    # (validation only: the exchange then goes through host copies)
+    backend = os.environ.get("GSP_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg = datagen.CONFIGS[args.config]
     assert cfg.H > 0, "bench step needs a config with the GAT chain (reddit / pubmed)"
     F, H = cfg.H * cfg.Fh, cfg.H
@@ -271,9 +279,23 @@ def main_gsp(args):
     OPS = op_list()
 
     def exchange():
-        for o, gbuf in zip(outs[:3], gathered[:3]):
-            dist.all_gather_into_tensor(gbuf, o)
-        dist.reduce_scatter_tensor(outs[3], partial)
+        if backend == "nccl":
+            for o, gbuf in zip(outs[:3], gathered[:3]):
+                dist.all_gather_into_tensor(gbuf, o)
+            dist.reduce_scatter_tensor(outs[3], partial)
+        else:   # host-staged equivalent (validation on a 1-GPU box)
+            for o, gbuf in zip(outs[:3], gathered[:3]):
+                parts = [torch.empty((R, F)) for _ in range(P)]
+                dist.all_gather(parts, o.cpu())
+                gbuf.copy_(torch.cat(parts))
+            t = partial.cpu()
+            dist.all_reduce(t)
+            outs[3].copy_(t[rank * R:(rank + 1) * R])
+
+    def allreduce_max(v):
+        t = torch.tensor([float(v)], device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     def step(record):
         def mark():
@@ -320,10 +342,31 @@ def main_gsp(args):
 
     t_step = sum(step_ms) / len(step_ms)
     if P > 1:
-        t = torch.tensor([t_step], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_step = float(t.item())
+        t_step = allreduce_max(t_step)
     value = N_OPS * E / (t_step * 1e-3) / 1e9
+
+    # ------------------------------------------- N > 1: check vs the full graph
+    check = None
+    if P > 1 and args.check:
+        step(False)
+        torch.cuda.synchronize()
+        def unpad(t):
+            return torch.cat([t[p * R:p * R + b[p + 1] - b[p]] for p in range(P)])
+        Xf, dYf, Zf, dOf = (unpad(t) for t in (X, dY, Z, dO))
+        ref1 = G.gspmm(Xf, gsp.NORM_BOTH)
+        ref2 = G.gspmm(dYf, gsp.NORM_BOTH, reverse=True)
+        sf = G.gsddmm(Zf, Zf, H=H)
+        G.edge_softmax(sf, out=sf)
+        ref3 = G.gspmm_weighted(Zf, sf)
+        ref4 = G.gspmm_weighted(dOf, sf, reverse=True)
+        def rel(a, ref):
+            return float((a - ref).abs().max() / (ref.abs().max() + 1e-30))
+        lo, hi = b[rank], b[rank + 1]
+        errs = [rel(unpad(gathered[0]), ref1), rel(unpad(gathered[1]), ref2), rel(unpad(gathered[2]), ref3),
+                rel(outs[3][:hi - lo], ref4[lo:hi])]
+        m = allreduce_max(max(errs))
+        check = {"max_rel_err_vs_single_gpu": m, "ok": bool(m < 1e-5)}
+        del ref1, ref2, ref3, ref4, sf, Xf, dYf, Zf, dOf
 
     # ---------------------------------------------------------------- e2e
     e2e = None
@@ -389,9 +432,7 @@ def main_gsp(args):
             e_ms.append(a0.elapsed_time(a1))
         t_e2e = sum(e_ms) / len(e_ms)
         if P > 1:
-            t = torch.tensor([t_e2e], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e = float(t.item())
+            t_e2e = allreduce_max(t_e2e)
         e2e = {"value": round(N_OPS * E / (t_e2e * 1e-3) / 1e9, 4), "unit": "GE/s",
                "ms_per_step": round(t_e2e, 4),
                "h2d_bytes_per_step": int(sum(h.numel() * 4 for h in hin)),
@@ -455,7 +496,8 @@ def main_gsp(args):
                      "frac_of_8TBs": round(gbs / 8000.0, 4)}
     if P > 1:
         per_op["exchange"] = {"ms": round(avg["exchange"], 4),
-                              "what": "3 x all_gather_into_tensor [R,F] + reduce_scatter_tensor [P*R,F] (NCCL)"}
+                              "what": "3 x all_gather_into_tensor [R,F] + reduce_scatter_tensor [P*R,F] "
+                                      + ("(NCCL)" if backend == "nccl" else "(host-staged gloo: validation only)")}
     dom = "gspmm_fwd"
     achieved = per_op[dom]["GB_s"]
     roofline = {"bound": "hbm", "kernel": "spmm_kernel<VEC=8,LPE=8,CPL=1,scaled> (gspmm fwd, BOTH norm)",
@@ -492,6 +534,7 @@ def main_gsp(args):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "next_rows": next_rows,
+            "multi_gpu_check": check,
             "e2e": e2e,
             "gpu_launches": (6 * args.steps),
             "clocks": clk,

@@ -140,3 +140,23 @@ def test_kron25_billion_edges():
     del out, X
     ref, T = oracle.gspmm_rows_coo(V, src, dst, Xh, 2, rows, F=cfg.F)
     within(got, ref, T)
+
+
+def test_bench_multi_rank_path_matches_single_gpu(tmp_path):
+    """bench.py's N > 1 path (destination-row partitions, all-gathers of the GCN /
+    GAT forward outputs, reduce-scatter of the GAT backward partials) run as 3
+    ranks sharing this GPU (gloo, host-staged exchange) must reproduce the
+    single-GPU results (--check)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GSP_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "3",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"), "--gpus", "3",
+           "--config", "pubmed", "--steps", "3", "--warmup", "3", "--check", "--no-e2e"]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 3 and line["multi_gpu_check"]["ok"], line["multi_gpu_check"]
