@@ -1,0 +1,46 @@
+"""Run every kernel family once on small graphs (for compute-sanitizer)."""
+import os, sys
+import numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import datagen, paper_2402_03548_b200 as gsp
+
+def run(V, src, dst, F=64, H=8):
+    g = gsp.Graph(V, src, dst, device=0)
+    X = torch.from_numpy(datagen.uniform(1, V, F)).cuda()
+    for norm in (0, 1, 2):
+        for rev in (0, 1):
+            g.gspmm(X, norm, reverse=rev)
+    for red in (1, 2):
+        g.gspmm_reduce(X, red)
+    s = g.gsddmm(X, X, H=H)
+    g.edge_softmax(s, out=s)
+    g.gspmm_weighted(X, s)
+    g.gspmm_weighted(X, s, reverse=True)
+    g.edge_softmax_backward(s, s.clone())
+    g.gat_forward(X, X, X, H)
+    g.gspmm_e(s, 0)
+    g.gspmm_e(s, 2, reverse=True)
+    g.gsddmm_ve(X[:, :H], s, 0, 1)
+    # odd shapes (generic / scalar paths)
+    X3 = torch.from_numpy(datagen.uniform(2, V, 15)).cuda()
+    g.gspmm(X3, 2)
+    s3 = g.gsddmm(X3, X3, H=3)
+    g.edge_softmax(s3)
+    g.gspmm_weighted(X3, s3)
+    g.gspmm_weighted(X3, s3, reverse=True)
+    P = 3
+    parts = [g.partition(P, p, device=0) for p in range(P)]
+    R = parts[0].R
+    Xp = torch.zeros((P * R, F), device="cuda")
+    for pg in parts:
+        pg.gspmm(Xp, 2)
+        a = pg.gsddmm(Xp, Xp, H=H)
+        pg.gspmm_weighted(Xp, a)
+        pg.gspmm_weighted(Xp, a, reverse=True)
+    torch.cuda.synchronize()
+
+V, src, dst = datagen.make_graph("cora")
+run(V, src, dst)
+src, dst = datagen.skewed_multigraph(1500, 60000, 3, alpha=1.6)   # heavy (CTA-split) rows
+run(1500, src, dst)
+print("sanitize workload done")
