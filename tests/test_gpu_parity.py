@@ -511,3 +511,49 @@ def test_gsddmm_ve(gsp, H):
     row_of = np.repeat(np.arange(V), np.diff(og.fwd_off))
     ref = (a_dst[row_of].astype(np.float32) + a_src[og.fwd_col].astype(np.float32))
     assert np.array_equal(e.cpu().numpy(), ref)
+
+
+# ------------------------------------------------ tile / bin boundary degrees
+def _boundary_graph():
+    """Destination rows with degrees exactly at the kernels' tile (32), fold
+    (4 x 32) and heavy-bin (1024) boundaries, plus empty rows; sources random."""
+    degs = [0, 1, 2, 31, 32, 33, 63, 64, 65, 127, 128, 129, 1023, 1024, 1025, 2047, 2048, 4097, 0, 7]
+    V = 300
+    rng = np.random.default_rng(5)
+    dst = np.concatenate([np.full(d, v, np.int64) for v, d in enumerate(degs)])
+    src = rng.integers(0, V, size=len(dst)).astype(np.int64)
+    perm = rng.permutation(len(dst))
+    return V, src[perm], dst[perm]
+
+
+def test_boundary_degrees_all_ops(gsp):
+    V, src, dst = _boundary_graph()
+    G, og = graph_pair(gsp, V, src, dst)
+    E = og.E
+    for F in (16, 64, 100):
+        Xh = datagen.uniform(F, V, F, lo=0.0, hi=1.0)
+        for norm in NORMS:
+            for rev in (0, 1):
+                ref, T = og.gspmm(Xh, norm, bool(rev))
+                assert_within(G.gspmm(dev(Xh), norm, reverse=rev).cpu().numpy(), ref, T, f"F{F} n{norm} r{rev}")
+        for red in (gsp.REDUCE_MIN, gsp.REDUCE_MAX):
+            ref, _ = og.gspmm_reduce(Xh, red)
+            assert np.array_equal(G.gspmm_reduce(dev(Xh), red).cpu().numpy().astype(np.float64), ref)
+    H, Fh = 8, 8
+    Zh = datagen.uniform(1, V, H * Fh)
+    wh = datagen.uniform(2, E, H, lo=0, hi=1)
+    for rev in (0, 1):
+        ref, T = og.gspmm_weighted(Zh, wh, bool(rev))
+        assert_within(G.gspmm_weighted(dev(Zh), dev(wh), reverse=rev).cpu().numpy(), ref, T, f"w r{rev}")
+    ref, T = og.gsddmm(Zh, Zh, H)
+    assert_within(G.gsddmm(dev(Zh), dev(Zh), H=H).cpu().numpy(), ref, T, "gsddmm")
+    lh = datagen.uniform(3, E, H, lo=-9, hi=9)
+    ah = og.edge_softmax(lh)
+    assert_within(G.edge_softmax(dev(lh)).cpu().numpy(), ah, 1.0, "softmax")
+    gh = datagen.uniform(4, E, H)
+    ref, T = og.edge_softmax_backward(ah.astype(np.float32), gh)
+    assert_within(G.edge_softmax_backward(dev(ah.astype(np.float32)), dev(gh)).cpu().numpy(), ref, T, "sbwd")
+    a_ref, o_ref, T = og.gat_forward(Zh, Zh, Zh, H)
+    alpha, out = G.gat_forward(dev(Zh), dev(Zh), dev(Zh), H)
+    assert_within(alpha.cpu().numpy(), a_ref, 1.0, "gat alpha")
+    assert_within(out.cpu().numpy(), o_ref, T, "gat out", scale=2e-5)
