@@ -192,6 +192,65 @@ def cpu_oracle_bench(V, src, dst, cfg, target_edges, steps=1, warmup=0):
 
 
 # ------------------------------------------------------------------ GPU arm
+def small_config_latency(gsp, torch):
+    """Cora GCN fwd+bwd (F=16) and Pubmed GAT chain (8x8): microseconds per step,
+    eager vs the same calls captured in one CUDA graph (the launch-bound regime of
+    P:1632-1688)."""
+    res = {}
+    st = torch.cuda.Stream()
+    for name in ("cora", "pubmed"):
+        cfg = datagen.CONFIGS[name]
+        V, src, dst = datagen.make_graph(cfg)
+        G = gsp.Graph(V, src, dst, device=torch.cuda.current_device())
+        F = cfg.F
+        X = torch.from_numpy(datagen.uniform(1, V, F)).cuda()
+        o1 = torch.empty((V, F), device="cuda")
+        o2 = torch.empty((V, F), device="cuda")
+        if name == "cora":
+            def stepf():
+                G.gspmm(X, gsp.NORM_BOTH, out=o1, stream=st)
+                G.gspmm(o1, gsp.NORM_BOTH, out=o2, reverse=True, stream=st)
+            n_ops = 2
+        else:
+            s = torch.empty((G.E, cfg.H), device="cuda")
+            def stepf():
+                G.gsddmm(X, X, out=s, stream=st)
+                G.edge_softmax(s, out=s, stream=st)
+                G.gspmm_weighted(X, s, out=o1, stream=st)
+            n_ops = 3
+        with torch.cuda.stream(st):
+            for _ in range(5):
+                stepf()
+        torch.cuda.synchronize()
+        reps = 200
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(st)
+        with torch.cuda.stream(st):
+            for _ in range(reps):
+                stepf()
+        a1.record(st)
+        torch.cuda.synchronize()
+        eager = a0.elapsed_time(a1) * 1e3 / reps
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=st):
+            stepf()
+        for _ in range(3):
+            gr.replay()
+        torch.cuda.synchronize()
+        a0.record(st)
+        with torch.cuda.stream(st):
+            for _ in range(reps):
+                gr.replay()
+        a1.record(st)
+        torch.cuda.synchronize()
+        graph = a0.elapsed_time(a1) * 1e3 / reps
+        res[name] = {"ops": "gspmm fwd+rev (BOTH), F=16" if name == "cora" else "gsddmm+softmax+weighted, 8x8",
+                     "n_kernels": n_ops, "eager_us_per_step": round(eager, 2), "cuda_graph_us_per_step": round(graph, 2),
+                     "V": V, "E": int(G.E)}
+    return res
+
+
+
 def main_gsp(args):
     import torch
     import torch.distributed as dist
@@ -438,6 +497,11 @@ def main_gsp(args):
                "h2d_bytes_per_step": int(sum(h.numel() * 4 for h in hin)),
                "d2h_bytes_per_step": int(sum(h.numel() * 4 for h in hout))}
 
+    # ------------------------- launch-bound configs (BASELINE configs[0], [1])
+    latency = None
+    if rank == 0 and not args.profile:
+        latency = small_config_latency(gsp, torch)
+
     # ----------------------------------------------------------- roofline
     peak, peak_kind = load_peaks()
     avg = {k: (sum(v) / len(v) if v else None) for k, v in ev.items()}
@@ -535,6 +599,7 @@ def main_gsp(args):
             "cpu_baseline": cpu,
             "next_rows": next_rows,
             "multi_gpu_check": check,
+            "small_config_latency": latency,
             "e2e": e2e,
             "gpu_launches": (6 * args.steps),
             "clocks": clk,

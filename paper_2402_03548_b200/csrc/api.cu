@@ -177,6 +177,12 @@ gsp_status check_compute_graph(const gsp_graph *g) {
 
 gsp_status check_stream(const gsp_graph *g, gsp_stream s) {
     if (!s) return GSP_OK;
+    // during CUDA-graph capture the stream cannot be queried (and the capture
+    // would be invalidated): skip the device check, everything else is capturable
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing((cudaStream_t)s, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+        return GSP_OK;
+    cudaGetLastError();
     int dev = -1;
     cudaError_t e = cudaStreamGetDevice((cudaStream_t)s, &dev);
     if (e != cudaSuccess) {

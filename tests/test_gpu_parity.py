@@ -557,3 +557,39 @@ def test_boundary_degrees_all_ops(gsp):
     alpha, out = G.gat_forward(dev(Zh), dev(Zh), dev(Zh), H)
     assert_within(alpha.cpu().numpy(), a_ref, 1.0, "gat alpha")
     assert_within(out.cpu().numpy(), o_ref, T, "gat out", scale=2e-5)
+
+
+def test_cuda_graph_capture_replay(gsp):
+    """Compute calls allocate nothing and never synchronise, so a whole GCN +
+    GAT step can be captured into a CUDA graph (the launch-bound Cora / Pubmed
+    regime, SURVEY §7 hard part 6) and replayed with identical results."""
+    cfg = datagen.CONFIGS["pubmed"]
+    V, src, dst = datagen.make_graph(cfg)
+    G = gsp.Graph(V, src, dst, device=0)
+    X = dev(datagen.uniform(1, V, 64))
+    o1 = torch.empty((V, 64), device="cuda")
+    o2 = torch.empty((V, 64), device="cuda")
+    o3 = torch.empty((V, 64), device="cuda")
+    s = torch.empty((G.E, 8), device="cuda")
+    st = torch.cuda.Stream()
+
+    def step():
+        G.gspmm(X, gsp.NORM_BOTH, out=o1, stream=st)
+        G.gspmm(o1, gsp.NORM_BOTH, out=o2, reverse=True, stream=st)
+        G.gsddmm(X, X, out=s, stream=st)
+        G.edge_softmax(s, out=s, stream=st)
+        G.gspmm_weighted(X, s, out=o3, stream=st)
+
+    with torch.cuda.stream(st):
+        step()
+    torch.cuda.synchronize()
+    ref = [t.clone() for t in (o1, o2, o3, s)]
+    for t in (o1, o2, o3, s):
+        t.zero_()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=st):
+        step()
+    gr.replay()
+    torch.cuda.synchronize()
+    for a, b in zip((o1, o2, o3, s), ref):
+        assert torch.equal(a, b)
