@@ -72,9 +72,12 @@ enum { GSP_NORM_NONE = 0, GSP_NORM_RIGHT = 1, GSP_NORM_BOTH = 2 };
 /* gsp_graph_create flags */
 enum {
     GSP_BUILD_REVERSE = 1u << 0,          /* build the rev (CSC) structure + rev_eid (needed for reverse=1) */
-    GSP_BUILD_SHARE_SYMMETRIC = 1u << 1   /* if the edge multiset is symmetric, keep ONE topology for
+    GSP_BUILD_SHARE_SYMMETRIC = 1u << 1,  /* if the edge multiset is symmetric, keep ONE topology for
                                              fwd and rev ("one copy of the topology"); rev_eid
                                              is still stored */
+    GSP_BUILD_EDGE_SCALES = 1u << 2       /* precompute the per-edge column-side degree scale of the BOTH
+                                             norm (4 B per edge per structure; one array when symmetric)
+                                             so gsp_gspmm streams it instead of gathering d^-1/2 per edge */
 };
 
 /* gsp_graph_partition flags */

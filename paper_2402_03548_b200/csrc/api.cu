@@ -262,6 +262,24 @@ static gsp_status upload_full(gsp_graph *g) {
         g->rev.col_scale[GSP_NORM_RIGHT] = inv_in;
         g->rev.col_scale[GSP_NORM_BOTH] = rsq_in;
     }
+    if (g->edge_scales) {
+        float *es = nullptr;
+        if ((st = dev_alloc_f32(g, (size_t)h.E, &es)) != GSP_OK) return st;
+        cudaError_t e0 = gsp::launch_gather_scale(g->fwd.col, h.E, rsq_out, es, 0);
+        if (e0 != cudaSuccess) return cuda_fail(e0, "edge scales");
+        g->fwd.edge_scale[GSP_NORM_BOTH] = es;
+        if (h.has_rev) {
+            if (h.symmetric) {
+                g->rev.edge_scale[GSP_NORM_BOTH] = es;   // d_in == d_out: the same values
+            } else {
+                float *er = nullptr;
+                if ((st = dev_alloc_f32(g, (size_t)h.E, &er)) != GSP_OK) return st;
+                e0 = gsp::launch_gather_scale(g->rev.col, h.E, rsq_in, er, 0);
+                if (e0 != cudaSuccess) return cuda_fail(e0, "edge scales");
+                g->rev.edge_scale[GSP_NORM_BOTH] = er;
+            }
+        }
+    }
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "graph upload");
     return GSP_OK;
@@ -273,7 +291,7 @@ gsp_status gsp_graph_create(int64_t V, int64_t E, const int64_t *src, const int6
     *g_out = nullptr;
     if (E > 0 && (!src || !dst)) return fail(GSP_ERR_NULL, "src/dst is NULL");
     if (V < 0 || E < 0) return fail(GSP_ERR_ARG, "V and E must be >= 0");
-    if (flags & ~(uint32_t)(GSP_BUILD_REVERSE | GSP_BUILD_SHARE_SYMMETRIC))
+    if (flags & ~(uint32_t)(GSP_BUILD_REVERSE | GSP_BUILD_SHARE_SYMMETRIC | GSP_BUILD_EDGE_SCALES))
         return fail(GSP_ERR_ARG, "unknown flags");
     if (V >= (int64_t(1) << 31) || E >= (int64_t(1) << 31))
         return fail(GSP_ERR_OVERFLOW, "V and E must be < 2^31 (int32 column and edge ids)");
@@ -302,6 +320,7 @@ gsp_status gsp_graph_create(int64_t V, int64_t E, const int64_t *src, const int6
     g->R = V;
     g->symmetric = g->host.symmetric;
     g->device = device;
+    g->edge_scales = (flags & GSP_BUILD_EDGE_SCALES) != 0;
     if (device >= 0) {
         st = upload_full(g);
         if (st != GSP_OK) {
@@ -370,7 +389,7 @@ gsp_status gsp_gspmm(const gsp_graph *g, const gsp_tensor *X, int norm, gsp_tens
     a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
     a.out = static_cast<float *>(out->data); a.ldo = out->ld;
     a.F = X->cols;
-    a.row_scale = S.row_scale[norm]; a.col_scale = S.col_scale[norm];
+    a.row_scale = S.row_scale[norm]; a.col_scale = S.col_scale[norm]; a.edge_scale = S.edge_scale[norm];
     a.H = 1; a.Fh = X->cols > 0 ? X->cols : 1;
     cudaError_t e = gsp::launch_spmm(a, gsp::kSpmmScaled, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "gspmm launch");
@@ -784,6 +803,21 @@ gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int dev
             if (st == GSP_OK && !prev) {
                 st = upload_structure(pg, pg->lrev, (int64_t)nparts * R, (int64_t)nparts * R, lh.rev_off, lh.rev_col,
                                       &lh.rev_eid, nullptr, 0, nullptr);
+            }
+            if (st == GSP_OK && g->edge_scales && lh.E > 0) {
+                pg->edge_scales = true;
+                float *es = nullptr;
+                if ((st = dev_alloc_f32(pg, (size_t)lh.E, &es)) == GSP_OK) {
+                    // fwd partition: column side = sources (d_out); reverse partition: destinations (d_in)
+                    const gsp::DevStructure &own = prev ? pg->rev : pg->fwd;
+                    cudaError_t e0 = gsp::launch_gather_scale(own.col, lh.E, prev ? pi_rsq : po_rsq, es, 0);
+                    if (e0 != cudaSuccess) st = cuda_fail(e0, "edge scales");
+                    if (prev) pg->rev.edge_scale[GSP_NORM_BOTH] = es;
+                    else {
+                        pg->fwd.edge_scale[GSP_NORM_BOTH] = es;
+                        if (h.symmetric) pg->rev.edge_scale[GSP_NORM_BOTH] = es;   // same values (d_in == d_out)
+                    }
+                }
             }
             if (st == GSP_OK) {
                 cudaError_t e = cudaDeviceSynchronize();

@@ -43,6 +43,8 @@ struct DevStructure {
     // degree scales per norm: index 0 NONE (null), 1 RIGHT, 2 BOTH; null => 1.0
     const float *row_scale[3] = {nullptr, nullptr, nullptr};
     const float *col_scale[3] = {nullptr, nullptr, nullptr};
+    // optional per-slot column scales (GSP_BUILD_EDGE_SCALES): edge_scale[n][j] = col_scale[n][col[j]]
+    const float *edge_scale[3] = {nullptr, nullptr, nullptr};
     // degree-binned schedule: rows by descending degree; the first n_heavy
     // rows get a whole CTA each, the rest one warp each.
     const int32_t *order = nullptr;
@@ -72,4 +74,5 @@ struct gsp_graph {
     gsp::DevStructure fwd, rev, lrev;
     std::vector<void *> dev_allocs;
     int64_t device_bytes = 0;
+    bool edge_scales = false;
 };

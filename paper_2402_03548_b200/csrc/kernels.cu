@@ -90,6 +90,12 @@ __device__ __forceinline__ void ld_stream_v8(float *d, const float *p, uint64_t 
     d[4] = __uint_as_float(u4); d[5] = __uint_as_float(u5); d[6] = __uint_as_float(u6); d[7] = __uint_as_float(u7);
 }
 
+__device__ __forceinline__ float ld_stream_f32(const float *p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 // async global -> shared copies (LDGSTS): edge-value rows land in smem without
 // occupying registers; src_size 0 zero-fills (padding lanes)
 __device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, int src_size) {
@@ -193,6 +199,10 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     constexpr int WS = W ? 2 * kWarps * 32 * kHMax : 0;   // double-buffered weight rows
     __shared__ __align__(16) int2 s_pair[kWarps][32];
     __shared__ __align__(16) float s_raw[RED > WS ? RED : WS];   // weights during the walk, then heavy combine
+    // Kahan compensation of narrow lanes lives in smem (touched once per fold):
+    // the registers go to gathers in flight
+    constexpr bool CMP_SMEM = VEC * CPL <= 8 && !MM;
+    __shared__ __align__(16) float s_cmp[CMP_SMEM ? kWarps : 1][CMP_SMEM ? 32 : 1][CMP_SMEM ? VEC * CPL : 1];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / LPE, sub = lane % LPE;
@@ -202,6 +212,9 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     bool heavy;
     if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     const Pol pol = make_pol();
+    float rs = 1.f;   // row scale, fetched up front (its latency hides under the row's gathers)
+    if constexpr (MODE == kSpmmScaled)
+        if (a.row_scale) rs = __ldg(a.row_scale + row);
 
     // lane constants: feature chunk q covers [f, f + VEC) of head hq
     const char *xl[CPL];
@@ -225,10 +238,15 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     // running sum (acc, cmp): error O((128/G) u) relative to sum|terms|,
     // independent of the row length.
     constexpr int NT = VEC >= 4 ? 1 : 2;   // independent tile accumulators (ILP for narrow lanes)
-    Vec<VEC> acc[CPL], cmp[CPL], tile[NT][CPL];
+    Vec<VEC> acc[CPL], cmp_r[CMP_SMEM ? 1 : CPL], tile[NT][CPL];
+    auto cmp_ref = [&](int q, int t) -> float & {
+        if constexpr (CMP_SMEM) return s_cmp[warp][lane][q * VEC + t];
+        else return cmp_r[q].v[t];
+    };
 #pragma unroll
     for (int q = 0; q < CPL; q++) {
-        vzero(cmp[q]);
+#pragma unroll
+        for (int t = 0; t < VEC; t++) cmp_ref(q, t) = 0.f;
 #pragma unroll
         for (int t = 0; t < VEC; t++) {
             acc[q].v[t] = ID;
@@ -254,7 +272,11 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     };
     auto load_scale = [&](int64_t tb, int c) -> float {
         if constexpr (MODE == kSpmmScaled) {
-            if (tb + lane < e) return HAS_CS ? __ldg(a.col_scale + c) : 1.f;
+            if (tb + lane < e) {
+                if constexpr (!HAS_CS) return 1.f;
+                // per-edge scales: one coalesced stream instead of a gather per edge
+                return a.edge_scale ? ld_stream_f32(a.edge_scale + tb + lane, pol.stream) : __ldg(a.col_scale + c);
+            }
         }
         return 0.f;
     };
@@ -377,9 +399,9 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
                     } else {
                         float y = tile[0][q].v[t];
                         if constexpr (NT == 2) y += tile[1][q].v[t];
-                        y -= cmp[q].v[t];
+                        y -= cmp_ref(q, t);
                         const float sum = acc[q].v[t] + y;
-                        cmp[q].v[t] = (sum - acc[q].v[t]) - y;
+                        cmp_ref(q, t) = (sum - acc[q].v[t]) - y;
                         acc[q].v[t] = sum;
                     }
 #pragma unroll
@@ -393,15 +415,11 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     for (int q = 0; q < CPL; q++)
 #pragma unroll
         for (int t = 0; t < VEC; t++) {
-            float v = acc[q].v[t] - cmp[q].v[t];
+            float v = acc[q].v[t] - cmp_ref(q, t);
 #pragma unroll
             for (int o = LPE; o < 32; o <<= 1) v = comb(v, __shfl_xor_sync(kFull, v, o));
             acc[q].v[t] = v;
         }
-
-    float rs = 1.f;
-    if constexpr (MODE == kSpmmScaled)
-        if (a.row_scale) rs = __ldg(a.row_scale + row);
 
     if (!heavy) {
         if (g == 0) {
@@ -1083,6 +1101,11 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_generic_kernel(const Sof
     }
 }
 
+__global__ void gather_scale_kernel(const int32_t *col, int64_t nnz, const float *scale, float *out) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x)
+        out[j] = scale[col[j]];
+}
+
 __global__ void degree_scales_kernel(const int64_t *deg, int64_t n, float *inv, float *rsq) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double d = deg[i] < 1 ? 1.0 : (double)deg[i];   // clamp d^ = max(d, 1)
@@ -1108,7 +1131,7 @@ template <int VEC, int LPE, int CPL, int UOVR = 0, int MINB = 0>
 cudaError_t spmm_go_v(const SpmmArgs &a, int mode, int64_t slabs, cudaStream_t s) {
     const dim3 grid = row_grid(a.nrows, a.n_heavy, slabs);
     if (mode == kSpmmScaled) {
-        if (a.col_scale) spmm_kernel<VEC, LPE, CPL, kSpmmScaled, true, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
+        if (a.col_scale || a.edge_scale) spmm_kernel<VEC, LPE, CPL, kSpmmScaled, true, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
         else spmm_kernel<VEC, LPE, CPL, kSpmmScaled, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
     } else if (mode == kSpmmWeightedFwd) {
         spmm_kernel<VEC, LPE, CPL, kSpmmWeightedFwd, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
@@ -1329,6 +1352,13 @@ cudaError_t launch_spmm_e(const SpmmEArgs &a, cudaStream_t s) {
 cudaError_t launch_sddmm_ve(const SddmmVeArgs &a, cudaStream_t s) {
     if (a.nrows == 0 || a.H == 0) return cudaSuccess;
     sddmm_ve_kernel<<<(unsigned)ceil_div(a.nrows, kWarps), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_scale(const int32_t *col, int64_t nnz, const float *scale, float *out, cudaStream_t s) {
+    if (nnz == 0) return cudaSuccess;
+    const int64_t blocks = ceil_div(nnz, 256) < 8192 ? ceil_div(nnz, 256) : 8192;
+    gather_scale_kernel<<<(unsigned)blocks, 256, 0, s>>>(col, nnz, scale, out);
     return cudaGetLastError();
 }
 

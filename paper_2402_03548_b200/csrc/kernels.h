@@ -20,6 +20,7 @@ struct SpmmArgs {
     int64_t F;
     const float *row_scale;  // may be null (1.0)
     const float *col_scale;  // may be null (1.0)
+    const float *edge_scale; // per-slot column scale (precomputed, streamed); overrides col_scale
     const float *w;          // weighted modes
     int64_t ldw;
     int64_t H, Fh;
@@ -125,6 +126,9 @@ struct SddmmVeArgs {
     int side_src;            // 1: X indexed by the column (source), 0: by the row (destination)
 };
 cudaError_t launch_sddmm_ve(const SddmmVeArgs &a, cudaStream_t s);
+
+// out[j] = scale[col[j]] for j < nnz (per-edge column scales, built once at create)
+cudaError_t launch_gather_scale(const int32_t *col, int64_t nnz, const float *scale, float *out, cudaStream_t s);
 
 // fp32 degree scales from (clamped) integer degrees: inv = 1/d^, rsq = d^^-1/2
 // computed in fp64 then rounded once.

@@ -91,7 +91,8 @@ def test_gspmm_random_graphs(gsp, F, ld):
         E = int(rng.integers(0, 40000))
         src, dst = (datagen.random_multigraph(V, E, seed) if seed != 1
                     else datagen.skewed_multigraph(V, E, seed))
-        G, og = graph_pair(gsp, V, src, dst)
+        # seed 2: without precomputed per-edge scales (the per-edge gather path)
+        G, og = graph_pair(gsp, V, src, dst, edge_scales=(seed != 2))
         Xh = datagen.uniform(seed + 11, V, F)
         X = padded(Xh, ld)
         for norm in NORMS:
@@ -267,6 +268,7 @@ def test_partitions_simulated_on_one_gpu(gsp, name):
     for P in (2, 3, 4):
         for rev in ((0, 1) if not G.symmetric else (0,)):
             parts = [G.partition(P, p, device=0, reverse=bool(rev)) for p in range(P)]
+            assert all(pg.device_bytes > 0 for pg in parts)
             R = parts[0].R
             b = G.partition_bounds(P, bool(rev))
             Xpad = torch.zeros((P * R, F), device="cuda")

@@ -31,6 +31,9 @@ flush = torch.empty(512 << 18, device="cuda")
 ops = {
     "gspmm_fwd": lambda: G.gspmm(X, 2, out=out),
     "gspmm_rev": lambda: G.gspmm(X, 2, out=out, reverse=True),
+    "gspmm_none": lambda: G.gspmm(X, 0, out=out),
+    "gspmm_right": lambda: G.gspmm(X, 1, out=out),
+    "gspmm_max": lambda: G.gspmm_reduce(X, 2, out=out),
     "gsddmm": lambda: G.gsddmm(Z, Z, out=s),
     "edge_softmax": lambda: G.edge_softmax(s, out=s),
     "wfwd": lambda: G.gspmm_weighted(Z, s, out=outg),
