@@ -385,9 +385,12 @@ def main_gsp(args):
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
     step_ms = []
+    host_launch_ms = []
     for _ in range(args.steps):
         flush.fill_(1.0)                      # L2 flush between timed steps (outside the events)
+        h0 = time.perf_counter()
         marks = step(True)
+        host_launch_ms.append((time.perf_counter() - h0) * 1e3)
         torch.cuda.synchronize()
         names = op_names + (["exchange"] if P > 1 else [])
         for i, n in enumerate(names):
@@ -603,7 +606,8 @@ def main_gsp(args):
             "e2e": e2e,
             "gpu_launches": (6 * args.steps),
             "clocks": clk,
-            "timing": {"wall_s_timed_region": round(wall, 3), "graph_gen_s": round(t_gen, 2),
+            "timing": {"wall_s_timed_region": round(wall, 3),
+                       "host_launch_ms_per_step": round(sum(host_launch_ms) / len(host_launch_ms), 3), "graph_gen_s": round(t_gen, 2),
                        "graph_create_s": round(t_create, 2), "device_graph_bytes": G.device_bytes},
         }
         print(json.dumps(line), flush=True)
