@@ -223,18 +223,6 @@ static gsp_status upload_full(gsp_graph *g) {
     const gsp::HostGraph &h = g->host;
     DeviceGuard dg(g->device);
     if (!dg.ok) return fail(GSP_ERR_ARG, "cannot select device " + std::to_string(g->device));
-    if (const char *pm = getenv("GSP_L2_PERSIST_MB")) {   // experiment knob
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atol(pm) << 20);
-        cudaGetLastError();
-    }
-    if (const char *fg = getenv("GSP_L2_FETCH")) {        // experiment knob: L2 fetch granularity (bytes)
-        size_t before = 0, after = 0;
-        cudaDeviceGetLimit(&before, cudaLimitMaxL2FetchGranularity);
-        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atol(fg));
-        cudaDeviceGetLimit(&after, cudaLimitMaxL2FetchGranularity);
-        fprintf(stderr, "gsp: L2 fetch granularity %zu -> %zu\n", before, after);
-        cudaGetLastError();
-    }
     gsp_status st;
     std::vector<int64_t> din = degrees_of(h.fwd_off), dout;
     if (h.has_rev) dout = degrees_of(h.rev_off);
