@@ -1,0 +1,270 @@
+// Fused GAT forward (NEXT-2).
+#include "common.cuh"
+
+namespace gsp {
+namespace {
+
+// ===================================================== fused GAT forward
+// NEXT-2 ("18 kernels in each layer"; a fused forward is
+// legal only if it still materialises the state tensor alpha).  One pass per
+// destination row v: for each in-edge j = (u -> v) and head h (one lane per
+// head, Fh = 8 features per lane):
+//   s = <X[v,h], Y[u,h]>          -> written to alpha (raw) ;
+//   online softmax (m, S) and acc = sum exp(s - m) Vt[u,h]   (flash-style);
+// then out[v,h] = acc / S and the row's raw scores are re-read (L2-hot) and
+// overwritten with alpha = exp(s - m) / S.  Y and Vt may be the same table
+// (one gather serves both).  Heavy rows: CTA split + deterministic merge.
+template <int LPE, bool SAME>
+__global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a) {
+    constexpr int VEC = 8;
+    constexpr int G = 32 / LPE;
+    constexpr int PER = LPE;
+    constexpr int U = SAME ? (PER >= 8 ? 8 : PER) : (PER >= 4 ? 4 : PER);   // edges in flight per lane
+    __shared__ __align__(16) int s_col[kWarps][32];
+    // running Kahan state (acc, accc) per lane lives in smem: touched once per
+    // tile (fold) and on the rare max increase (rescale), keeping registers for
+    // the gathers in flight.  Reused for the heavy-row cross-warp merge.
+    __shared__ __align__(16) float s_run[kWarps][32][2 * VEC];
+    __shared__ float sm_ms[kWarps][LPE][2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPE, h = lane % LPE;   // head of this lane
+    const int H = LPE;
+
+    int64_t row, b, e;
+    bool heavy;
+    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    const Pol pol = make_pol();
+
+    Vec<VEC> xv;
+    ld_keep(xv, a.X + (a.row_base + row) * a.ldx + h * VEC, pol.stream);
+    const char *yl = reinterpret_cast<const char *>(a.Y + h * VEC);
+    const char *vl = reinterpret_cast<const char *>(a.Vt + h * VEC);
+    const uint32_t ldyb = (uint32_t)(a.ldy * 4), ldvb = (uint32_t)(a.ldv * 4);
+
+    // (m, S + Sc compensation) in registers; acc / accc in smem; tile sums in registers
+    float m = -INFINITY, S = 0.f, Sc = 0.f, St = 0.f;
+    float *run = s_run[warp][lane];
+#pragma unroll
+    for (int t = 0; t < 2 * VEC; t++) run[t] = 0.f;
+    Vec<VEC> acct;
+    vzero(acct);
+    int ntile = 0;
+
+    auto load_col = [&](int64_t tb) { return tb + lane < e ? ld_stream_i32(a.col + tb + lane, pol.stream) : 0; };
+    int c1 = load_col(b), c2 = load_col(b + 32);
+    for (int64_t base = b; base < e; base += 32) {
+        const int n = (int)(e - base < 32 ? e - base : 32);
+        s_col[warp][(lane % G) * PER + lane / G] = c1;
+        c1 = c2;
+        c2 = load_col(base + 64);
+        __syncwarp();
+        const int *gp = &s_col[warp][g * PER];
+        float *ab = a.alpha + (base + g) * H + h;   // group g's i-th edge is tile edge g + G*i
+        const int mcount = n == 32 ? PER : (n > g ? (n - g + G - 1) / G : 0);
+        auto body = [&](int i, auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
+            Vec<VEC> y[U], vv[SAME ? 1 : U];
+            int cc[U];
+            if constexpr (U % 4 == 0) {
+#pragma unroll
+                for (int u = 0; u < U; u += 4) {
+                    const int4 c4 = *reinterpret_cast<const int4 *>(gp + i + u);
+                    cc[u] = c4.x; cc[u + 1] = c4.y; cc[u + 2] = c4.z; cc[u + 3] = c4.w;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; u++) cc[u] = gp[i + u];
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (FULL || i + u < mcount) {
+                    ld_keep(y[u], reinterpret_cast<const float *>(yl + (uint64_t)(uint32_t)cc[u] * ldyb), pol.keep);
+                    if constexpr (!SAME)
+                        ld_keep(vv[u], reinterpret_cast<const float *>(vl + (uint64_t)(uint32_t)cc[u] * ldvb), pol.keep);
+                } else {
+                    vzero(y[u]);
+                    if constexpr (!SAME) vzero(vv[u]);
+                }
+            }
+            // scores of the batch, at most one rescale per batch, then the weights
+            float sc[U];
+            float mb = -INFINITY;
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                float s0 = 0.f, s1 = 0.f;   // two chains: shorter dependency
+#pragma unroll
+                for (int t = 0; t < VEC; t += 2) {
+                    s0 = fmaf(xv.v[t], y[u].v[t], s0);
+                    s1 = fmaf(xv.v[t + 1], y[u].v[t + 1], s1);
+                }
+                sc[u] = s0 + s1;
+                if (FULL || i + u < mcount) {
+                    ab[(int64_t)(G * (i + u)) * H] = sc[u];   // raw score (default L2 policy), re-read below
+                    mb = fmaxf(mb, sc[u]);
+                } else {
+                    sc[u] = -INFINITY;
+                }
+            }
+            // lazy rescale: the reference m moves only when a score exceeds it by
+            // more than 8 (exp(s - m) <= e^8 keeps every sum finite); the result
+            // exp(s - m) / sum exp(s - m) does not depend on the reference, and the
+            // (warp-divergent) branch is taken about once per row.
+            if (mb > m + 8.f) {
+                const float r = fast_exp(m - mb);   // 0 when m = -inf
+                S *= r; Sc *= r; St *= r;
+#pragma unroll
+                for (int t = 0; t < VEC; t++) {
+                    run[t] *= r;
+                    run[VEC + t] *= r;
+                    acct.v[t] *= r;
+                }
+                m = mb;
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const float pu = fast_exp(sc[u] - m);   // 0 for padding (-inf)
+                const Vec<VEC> &val = SAME ? y[u] : vv[SAME ? 0 : u];
+                St += pu;
+#pragma unroll
+                for (int t = 0; t < VEC; t++) acct.v[t] = fmaf(pu, val.v[t], acct.v[t]);
+            }
+        };
+        if (n == 32) {
+#pragma unroll 1
+            for (int i = 0; i < PER; i += U) body(i, std::true_type{});
+        } else {
+#pragma unroll 1
+            for (int i = 0; i < mcount; i += U) body(i, std::false_type{});
+        }
+        __syncwarp();
+        if (++ntile == kFoldTiles || base + 32 >= e) {   // Kahan fold of the tile sums
+            ntile = 0;
+            float y2 = St - Sc, t2 = S + y2;
+            Sc = (t2 - S) - y2; S = t2; St = 0.f;
+#pragma unroll
+            for (int t = 0; t < VEC; t++) {
+                const float ac = run[t], cc = run[VEC + t];
+                y2 = acct.v[t] - cc;
+                t2 = ac + y2;
+                run[VEC + t] = (t2 - ac) - y2;
+                run[t] = t2;
+                acct.v[t] = 0.f;
+            }
+        }
+    }
+    S -= Sc;
+    Vec<VEC> acc;
+#pragma unroll
+    for (int t = 0; t < VEC; t++) acc.v[t] = run[t] - run[VEC + t];
+    // merge the G edge groups (same head h): online-softmax merge
+    auto merge = [&](float mo, float So, const Vec<VEC> &ao) {
+        const float mn = fmaxf(m, mo);
+        if (mn == -INFINITY) return;
+        const float r1 = m == -INFINITY ? 0.f : fast_exp(m - mn), r2 = mo == -INFINITY ? 0.f : fast_exp(mo - mn);
+        S = S * r1 + So * r2;
+#pragma unroll
+        for (int t = 0; t < VEC; t++) acc.v[t] = acc.v[t] * r1 + ao.v[t] * r2;
+        m = mn;
+    };
+#pragma unroll
+    for (int o = LPE; o < 32; o <<= 1) {
+        Vec<VEC> ao;
+        const float mo = __shfl_xor_sync(kFull, m, o), So = __shfl_xor_sync(kFull, S, o);
+#pragma unroll
+        for (int t = 0; t < VEC; t++) ao.v[t] = __shfl_xor_sync(kFull, acc.v[t], o);
+        merge(mo, So, ao);
+    }
+    if (heavy) {
+        // every warp of the CTA holds (m, S, acc) of its slice per head: merge in warp order
+        __syncthreads();   // s_run is reused for the cross-warp state
+        if (g == 0) {
+            sm_ms[warp][h][0] = m;
+            sm_ms[warp][h][1] = S;
+#pragma unroll
+            for (int t = 0; t < VEC; t++) s_run[warp][h][t] = acc.v[t];
+        }
+        __syncthreads();
+        m = -INFINITY;
+        S = 0.f;
+        vzero(acc);
+        for (int w = 0; w < kWarps; w++) {
+            Vec<VEC> ao;
+#pragma unroll
+            for (int t = 0; t < VEC; t++) ao.v[t] = s_run[w][h][t];
+            merge(sm_ms[w][h][0], sm_ms[w][h][1], ao);
+        }
+    }
+    const float rS = S > 0.f ? 1.0f / S : 0.f;
+    if (g == 0 && (!heavy || warp == 0)) {
+        Vec<VEC> r;
+#pragma unroll
+        for (int t = 0; t < VEC; t++) r.v[t] = acc.v[t] * rS;
+        vstore(a.out + row * a.ldo + h * VEC, r, VEC);
+    }
+    // normalise this warp's slice of raw scores in place: element i has head i % H
+    __syncwarp();
+    const int64_t lo = b * H, hi = e * H;
+    if (H % 4 == 0) {
+        float mh[4], rh[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            const int hh = (lane * 4 + t) % H;
+            mh[t] = __shfl_sync(kFull, m, hh);
+            rh[t] = __shfl_sync(kFull, rS, hh);
+        }
+        constexpr int NU = 8;   // loads in flight per lane (the row block is L2-hot)
+        for (int64_t i0 = lo + (int64_t)lane * 4; i0 < hi; i0 += 128 * NU) {
+            float4 v[NU];
+#pragma unroll
+            for (int k = 0; k < NU; k++)
+                if (i0 + 128 * k < hi) v[k] = ld_f4(a.alpha + i0 + 128 * k, pol.stream);
+#pragma unroll
+            for (int k = 0; k < NU; k++)
+                if (i0 + 128 * k < hi)
+                    st_stream_f4(a.alpha + i0 + 128 * k,
+                                 make_float4(fast_exp(v[k].x - mh[0]) * rh[0], fast_exp(v[k].y - mh[1]) * rh[1],
+                                             fast_exp(v[k].z - mh[2]) * rh[2], fast_exp(v[k].w - mh[3]) * rh[3]),
+                                 pol.stream);
+        }
+    } else {
+        const int hh = lane % H;
+        const float mh = __shfl_sync(kFull, m, hh), rh = __shfl_sync(kFull, rS, hh);
+        for (int64_t i = lo + lane; i < hi; i += 32) {
+            const float v = ld_f32(a.alpha + i, pol.stream);
+            st_stream_f32(a.alpha + i, fast_exp(v - mh) * rh, pol.stream);
+        }
+    }
+}
+
+}  // namespace
+
+bool gat_fused_supported(const GatArgs &a) {
+    const int64_t H = a.H;
+    const bool h_ok = H == 2 || H == 4 || H == 8 || H == 16 || H == 32;
+    return h_ok && a.ldx % 8 == 0 && a.ldy % 8 == 0 && a.ldv % 8 == 0 && a.ldo % 4 == 0 && aligned(a.X, 32) &&
+           aligned(a.Y, 32) && aligned(a.Vt, 32) && aligned(a.out, 16) && aligned(a.alpha, 16);
+}
+
+cudaError_t launch_gat_fused(const GatArgs &a, cudaStream_t s) {
+    if (a.nrows == 0) return cudaSuccess;
+    const dim3 grid = row_grid(a.nrows, a.n_heavy, 1);
+    const bool same = a.Vt == a.Y && a.ldv == a.ldy;
+#define GSP_GAT_CASE(HH)                                                         \
+    case HH:                                                                     \
+        if (same) gat_fused_kernel<HH, true><<<grid, kThreads, 0, s>>>(a);       \
+        else gat_fused_kernel<HH, false><<<grid, kThreads, 0, s>>>(a);           \
+        break;
+    switch (a.H) {
+        GSP_GAT_CASE(2)
+        GSP_GAT_CASE(4)
+        GSP_GAT_CASE(8)
+        GSP_GAT_CASE(16)
+        default:
+            if (same) gat_fused_kernel<32, true><<<grid, kThreads, 0, s>>>(a);
+            else gat_fused_kernel<32, false><<<grid, kThreads, 0, s>>>(a);
+    }
+#undef GSP_GAT_CASE
+    return cudaGetLastError();
+}
+
+}  // namespace gsp

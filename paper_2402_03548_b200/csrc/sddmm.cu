@@ -1,0 +1,227 @@
+// gSDDMMvv (u.v scores) and gSDDMMve.
+#include "common.cuh"
+
+namespace gsp {
+namespace {
+
+// ================================================================ gSDDMMvv
+// out[j, h] = <X[row_base + v, head h], Y[col_j, head h]>; CPH = Fh / VEC lanes per head.
+template <int VEC, int LPE, int CPL, int CPH, int UOVR = 0, int MINB = 0>
+__global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 : 2))) sddmm_kernel(const SddmmArgs a) {
+    constexpr int G = 32 / LPE;
+    constexpr int PER = LPE;
+    constexpr int UB = 32 / (VEC * CPL);
+    constexpr int U0 = UOVR ? UOVR : (UB < 2 ? 2 : (UB > 4 ? 4 : UB));
+    constexpr int U = U0 > PER ? PER : U0;
+    constexpr int SW = VEC * LPE * CPL;
+    __shared__ __align__(16) int s_col[kWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPE, sub = lane % LPE;
+    const int64_t F = a.H * a.Fh;
+    const int64_t f0 = (int64_t)blockIdx.y * SW;
+
+    int64_t row, b, e;
+    bool heavy;
+    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    if (b >= e) return;
+    const Pol pol = make_pol();
+
+    const char *yl[CPL];
+    bool fv[CPL], wr[CPL];
+    int hq[CPL];
+    Vec<VEC> xv[CPL];
+    // the row's features are fetched once and reused for every edge
+    const float *xr = a.X + (a.row_base + row) * a.ldx;
+#pragma unroll
+    for (int q = 0; q < CPL; q++) {
+        const int64_t f = f0 + (int64_t)(sub + q * LPE) * VEC;
+        fv[q] = f < F;
+        yl[q] = reinterpret_cast<const char *>(a.Y + (fv[q] ? f : 0));
+        hq[q] = (int)((fv[q] ? f : 0) / a.Fh);
+        wr[q] = fv[q] && (sub % CPH) == 0;
+        if (fv[q]) ld_keep(xv[q], xr + f, pol.stream);
+        else vzero(xv[q]);
+    }
+    const uint32_t ldyb = (uint32_t)(a.ldy * 4);
+
+    // column ids are loaded two tiles ahead of their gathers (index pipeline)
+    auto load_col = [&](int64_t tb) { return tb + lane < e ? ld_stream_i32(a.col + tb + lane, pol.stream) : 0; };
+    int c1 = load_col(b), c2 = load_col(b + 32);
+    for (int64_t base = b; base < e; base += 32) {
+        const int n = (int)(e - base < 32 ? e - base : 32);
+        s_col[warp][(lane % G) * PER + lane / G] = c1;
+        c1 = c2;
+        c2 = load_col(base + 64);
+        __syncwarp();
+        const int *gp = &s_col[warp][g * PER];
+        float *ob = a.out + (base + g) * a.ldo;   // group g's i-th edge is tile edge g + G*i
+
+        auto body = [&](int i, bool full, int m) {
+            Vec<VEC> y[U][CPL];
+#pragma unroll
+            for (int u = 0; u < U; u += 2) {
+                const int2 cc = *reinterpret_cast<const int2 *>(gp + i + u);
+                const int c2[2] = {cc.x, cc.y};
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    const bool ok = full || (i + u + k < m);
+#pragma unroll
+                    for (int q = 0; q < CPL; q++) {
+                        if (ok && fv[q])
+                            ld_keep(y[u + k][q],
+                                    reinterpret_cast<const float *>(yl[q] + (uint64_t)(uint32_t)c2[k] * ldyb),
+                                    pol.keep);
+                        else vzero(y[u + k][q]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const bool ok = full || (i + u < m);
+#pragma unroll
+                for (int q = 0; q < CPL; q++) {
+                    float p = 0.f;
+#pragma unroll
+                    for (int t = 0; t < VEC; t++) p = fmaf(xv[q].v[t], y[u][q].v[t], p);
+#pragma unroll
+                    for (int o = 1; o < CPH; o <<= 1) p += __shfl_xor_sync(kFull, p, o);
+                    if (ok && wr[q]) st_stream_f32(ob + (int64_t)(G * (i + u)) * a.ldo + hq[q], p, pol.stream);
+                }
+            }
+        };
+        if (n == 32) {
+#pragma unroll 1
+            for (int i = 0; i < PER; i += U) body(i, true, PER);
+        } else {
+            const int m = n > g ? (n - g + G - 1) / G : 0;
+            // all lanes run the same trip count (the xor-shuffles need the full warp)
+            const int mmax = (n + G - 1) / G;
+#pragma unroll 1
+            for (int i = 0; i < mmax; i += U) body(i, false, m);
+        }
+        __syncwarp();
+    }
+}
+
+// generic gSDDMM for head shapes the vector path does not cover: one thread
+// per (edge, head), sequential dot over Fh.
+__global__ void __launch_bounds__(kThreads) sddmm_generic_kernel(const SddmmArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t row, b, e;
+    bool heavy;
+    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    const float *xr = a.X + (a.row_base + row) * a.ldx;
+    const int64_t tot = (e - b) * a.H;
+    for (int64_t t = lane; t < tot; t += 32) {
+        const int64_t j = b + t / a.H, h = t % a.H;
+        const float *yr = a.Y + (int64_t)__ldg(a.col + j) * a.ldy + h * a.Fh;
+        float p = 0.f;
+        for (int64_t f = 0; f < a.Fh; f++) p = fmaf(__ldg(xr + h * a.Fh + f), __ldg(yr + f), p);
+        a.out[j * a.ldo + h] = p;
+    }
+}
+
+// ========================================================= gSDDMMve (NEXT-3)
+// gSDDMMve: out[j,h] = w[j,h] OP X[side ? col_j : row_base + row, h]; out may be w (in place).
+__global__ void __launch_bounds__(kThreads) sddmm_ve_kernel(const SddmmVeArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t idx = (int64_t)blockIdx.x * kWarps + warp;
+    if (idx >= a.nrows) return;
+    const int64_t row = a.order[idx], b = a.off[row], e = a.off[row + 1];
+    const int64_t H = a.H;
+    const int64_t tot = (e - b) * H;
+    for (int64_t t = lane; t < tot; t += 32) {
+        const int64_t j = b + t / H, h = t % H;
+        const int64_t vx = a.side_src ? (int64_t)__ldg(a.col + j) : a.row_base + row;
+        const float x = __ldg(a.X + vx * a.ldx + h), wv = a.w[j * a.ldw + h];
+        float r;
+        switch (a.op) {
+            case 0: r = wv + x; break;
+            case 1: r = wv - x; break;
+            case 2: r = wv * x; break;
+            default: r = wv / x; break;
+        }
+        a.out[j * a.ldo + h] = r;
+    }
+}
+
+int tune_sddmm() {
+    static int v = [] {
+        const char *e = getenv("GSP_TUNE_SDDMM");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
+template <int VEC, int LPE, int CPL>
+cudaError_t sddmm_go_cph(const SddmmArgs &a, int cph, int64_t slabs, cudaStream_t s) {
+    const dim3 grid = row_grid(a.nrows, a.n_heavy, slabs);
+    if constexpr (VEC == 8 && LPE == 8 && CPL == 1) {
+        if (cph == 1) {
+            switch (tune_sddmm()) {
+                case 0:   // measured best on B200 (Reddit-shaped H = 8 x 8, tools/opbench.py)
+                case 2: sddmm_kernel<VEC, LPE, CPL, 1, 4, 4><<<grid, kThreads, 0, s>>>(a); return cudaGetLastError();
+                case 1: sddmm_kernel<VEC, LPE, CPL, 1, 8, 2><<<grid, kThreads, 0, s>>>(a); return cudaGetLastError();
+                case 3: sddmm_kernel<VEC, LPE, CPL, 1, 2, 4><<<grid, kThreads, 0, s>>>(a); return cudaGetLastError();
+                default: break;
+            }
+        }
+    }
+    switch (cph) {
+        case 1: sddmm_kernel<VEC, LPE, CPL, 1><<<grid, kThreads, 0, s>>>(a); break;
+        case 2: sddmm_kernel<VEC, LPE, CPL, (LPE >= 2 ? 2 : 1)><<<grid, kThreads, 0, s>>>(a); break;
+        case 4: sddmm_kernel<VEC, LPE, CPL, (LPE >= 4 ? 4 : 1)><<<grid, kThreads, 0, s>>>(a); break;
+        case 8: sddmm_kernel<VEC, LPE, CPL, (LPE >= 8 ? 8 : 1)><<<grid, kThreads, 0, s>>>(a); break;
+        case 16: sddmm_kernel<VEC, LPE, CPL, (LPE >= 16 ? 16 : 1)><<<grid, kThreads, 0, s>>>(a); break;
+        default: sddmm_kernel<VEC, LPE, CPL, 32><<<grid, kThreads, 0, s>>>(a); break;
+    }
+    return cudaGetLastError();
+}
+
+template <int VEC>
+cudaError_t sddmm_dispatch(const SddmmArgs &a, int cph, cudaStream_t s) {
+    const int64_t nch = ceil_div(a.H * a.Fh, VEC);
+    if (nch <= 16) {
+        // the lanes of one edge must cover a whole head: lpe >= cph
+        int lpe = pow2ceil(nch < 2 ? 2 : nch);
+        if (lpe < cph) lpe = cph;
+        if (lpe == 2) return sddmm_go_cph<VEC, 2, 1>(a, cph, 1, s);
+        if (lpe == 4) return sddmm_go_cph<VEC, 4, 1>(a, cph, 1, s);
+        if (lpe == 8) return sddmm_go_cph<VEC, 8, 1>(a, cph, 1, s);
+        if (lpe == 16) return sddmm_go_cph<VEC, 16, 1>(a, cph, 1, s);
+    }
+    constexpr int MAXCPL = VEC >= 8 ? 2 : 4;
+    const int64_t slabs = ceil_div(nch, 32 * MAXCPL);
+    const int64_t cpl = ceil_div(nch, 32 * slabs);
+    switch (cpl) {
+        case 1: return sddmm_go_cph<VEC, 32, 1>(a, cph, slabs, s);
+        case 2: return sddmm_go_cph<VEC, 32, 2>(a, cph, slabs, s);
+        default: return sddmm_go_cph<VEC, 32, MAXCPL>(a, cph, slabs, s);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_sddmm(const SddmmArgs &a, cudaStream_t s) {
+    if (a.nrows == 0 || a.H == 0) return cudaSuccess;
+    auto is_pow2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
+    auto ok_vec = [&](int v) {
+        return a.Fh % v == 0 && is_pow2(a.Fh / v) && a.Fh / v <= 32 && a.ldx % v == 0 && a.ldy % v == 0 &&
+               aligned(a.X, 4 * v) && aligned(a.Y, 4 * v);
+    };
+    if (ok_vec(8)) return sddmm_dispatch<8>(a, (int)(a.Fh / 8), s);
+    if (ok_vec(4)) return sddmm_dispatch<4>(a, (int)(a.Fh / 4), s);
+    if (ok_vec(1)) return sddmm_dispatch<1>(a, (int)a.Fh, s);
+    SddmmArgs g = a;
+    g.n_heavy = 0;
+    sddmm_generic_kernel<<<row_grid(a.nrows, 0, 1), kThreads, 0, s>>>(g);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sddmm_ve(const SddmmVeArgs &a, cudaStream_t s) {
+    if (a.nrows == 0 || a.H == 0) return cudaSuccess;
+    sddmm_ve_kernel<<<(unsigned)ceil_div(a.nrows, kWarps), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace gsp
