@@ -1,4 +1,4 @@
-// Host-side launchers of the sm_100a kernels (kernels.cu).  Internal.
+// Host-side launchers of the sm_100a kernels (spmm.cu, sddmm.cu, softmax.cu, gat.cu).  Internal.
 #pragma once
 #include <cuda_runtime.h>
 
