@@ -542,8 +542,13 @@ def main_gsp(args):
                                   "GE_s": round(Eloc / (ms_gat * 1e-3) / 1e9, 3)},
             "gspmm_reduce_max": {"row": "NEXT-3", "ms": round(ms_max, 4),
                                  "GB_s": round(alg_bytes("gspmm", Vloc, Eloc, F, H) / (ms_max * 1e-3) / 1e9, 1)},
-            "gspmm_e_sum": {"row": "NEXT-3", "ms": round(ms_e, 4)},
-            "gsddmm_ve_add_src": {"row": "NEXT-3", "ms": round(ms_ve, 4)},
+            # algorithmic bytes: w read once (+ row offsets, out) / w read + out
+            # written + col indices + the gathered X table read once
+            "gspmm_e_sum": {"row": "NEXT-3", "ms": round(ms_e, 4),
+                            "GB_s": round((Eloc * H * 4 + (Vloc + 1) * 8 + Vloc * H * 4) / (ms_e * 1e-3) / 1e9, 1)},
+            "gsddmm_ve_add_src": {"row": "NEXT-3", "ms": round(ms_ve, 4),
+                                  "GB_s": round((2 * Eloc * H * 4 + Eloc * 4 + (Vloc + 1) * 8 + V * H * 4)
+                                                / (ms_ve * 1e-3) / 1e9, 1)},
             "edge_softmax_backward": {"row": "NEXT-1", "ms": round(ms_sbw, 4),
                                       "GB_s": round(alg_bytes("edge_softmax", Vloc, Eloc, F, H) * 1.5 / (ms_sbw * 1e-3) / 1e9, 1)},
         }

@@ -608,7 +608,7 @@ gsp_status gsp_gspmm_e(const gsp_graph *g, const gsp_tensor *w, int reduce, gsp_
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SpmmEArgs a{};
-    a.off = S.off; a.eid = reverse ? S.eid : nullptr; a.order = S.order; a.nrows = S.nrows;
+    a.off = S.off; a.eid = reverse ? S.eid : nullptr; a.order = S.order; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
     a.w = static_cast<const float *>(w->data); a.ldw = w->ld;
     a.out = static_cast<float *>(out->data); a.ldo = out->ld;
     a.H = w->cols; a.red = reduce;
@@ -635,7 +635,8 @@ gsp_status gsp_gsddmm_ve(const gsp_graph *g, const gsp_tensor *X, const gsp_tens
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SddmmVeArgs a{};
-    a.off = S.off; a.col = S.col; a.order = S.order; a.nrows = S.nrows; a.row_base = g->row_base;
+    a.off = S.off; a.col = S.col; a.order = S.order; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.row_base = g->row_base;
     a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
     a.w = static_cast<const float *>(w->data); a.ldw = w->ld;
     a.out = static_cast<float *>(out->data); a.ldo = out->ld;

@@ -98,6 +98,14 @@ __device__ __forceinline__ float ld_stream_f32(const float *p, uint64_t pol) {
     return v;
 }
 
+// one streamed 16-byte vector (edge-value rows of H = 4k heads)
+__device__ __forceinline__ float4 ld_stream_f4(const float *p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+
 // async global -> shared copies (LDGSTS): edge-value rows land in smem without
 // occupying registers; src_size 0 zero-fills (padding lanes)
 __device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, int src_size) {

@@ -100,7 +100,7 @@ struct SpmmEArgs {
     const int64_t *off;
     const int32_t *eid;      // null: implicit (slot = edge id)
     const int32_t *order;
-    int64_t nrows;
+    int64_t nrows, n_heavy;  // rows in LPT order; the first n_heavy get a CTA each
     const float *w;
     int64_t ldw;
     float *out;
@@ -114,7 +114,7 @@ struct SddmmVeArgs {
     const int64_t *off;
     const int32_t *col;
     const int32_t *order;
-    int64_t nrows, row_base;
+    int64_t nrows, n_heavy, row_base;
     const float *X;
     int64_t ldx;
     const float *w;

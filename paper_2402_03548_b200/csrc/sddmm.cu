@@ -145,6 +145,70 @@ __global__ void __launch_bounds__(kThreads) sddmm_ve_kernel(const SddmmVeArgs a)
     }
 }
 
+// Vector path (H in {4, 8, 16, 32}, 16-B aligned rows): QH = H/4 lanes per edge,
+// one float4 of heads each; destination-side X row loaded once per warp.
+// In place (out == w) is safe: each element is read, then written, by the
+// same thread, through coherent loads.
+template <int QH, int OP, bool SRC>
+__global__ void __launch_bounds__(kThreads) sddmm_ve_vec_kernel(const SddmmVeArgs a) {
+    constexpr int EPW = 32 / QH, U = 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t row, b, e;
+    bool heavy;
+    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    const Pol pol = make_pol();
+    const int eo = lane / QH, q = lane % QH;
+    float4 xd = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!SRC && b < e) xd = __ldg(reinterpret_cast<const float4 *>(a.X + (a.row_base + row) * a.ldx + 4 * q));
+    auto apply = [](float w, float x) {
+        if constexpr (OP == 0) return w + x;
+        else if constexpr (OP == 1) return w - x;
+        else if constexpr (OP == 2) return w * x;
+        else return w / x;
+    };
+    auto one = [&](int64_t jj, const float4 wv, const float4 x) {
+        st_stream_f4(a.out + jj * a.ldo + 4 * q,
+                     make_float4(apply(wv.x, x.x), apply(wv.y, x.y), apply(wv.z, x.z), apply(wv.w, x.w)), pol.stream);
+    };
+    int64_t j = b + eo;
+    for (; j + (U - 1) * EPW < e; j += U * EPW) {
+        float4 wv[U], x[U];
+        if constexpr (SRC) {
+            int c[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) c[u] = __ldg(a.col + j + u * EPW);
+#pragma unroll
+            for (int u = 0; u < U; u++) x[u] = __ldg(reinterpret_cast<const float4 *>(a.X + (int64_t)c[u] * a.ldx + 4 * q));
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) wv[u] = ld_f4(a.w + (j + u * EPW) * a.ldw + 4 * q, pol.stream);
+#pragma unroll
+        for (int u = 0; u < U; u++) one(j + u * EPW, wv[u], SRC ? x[u] : xd);
+    }
+    for (; j < e; j += EPW) {
+        const float4 x = SRC ? __ldg(reinterpret_cast<const float4 *>(a.X + (int64_t)__ldg(a.col + j) * a.ldx + 4 * q)) : xd;
+        one(j, ld_f4(a.w + j * a.ldw + 4 * q, pol.stream), x);
+    }
+}
+
+template <int QH, int OP>
+cudaError_t sddmm_ve_side(const SddmmVeArgs &a, cudaStream_t s) {
+    const dim3 grid = row_grid(a.nrows, a.n_heavy, 1);
+    if (a.side_src) sddmm_ve_vec_kernel<QH, OP, true><<<grid, kThreads, 0, s>>>(a);
+    else sddmm_ve_vec_kernel<QH, OP, false><<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int QH>
+cudaError_t sddmm_ve_op(const SddmmVeArgs &a, cudaStream_t s) {
+    switch (a.op) {
+        case 0: return sddmm_ve_side<QH, 0>(a, s);
+        case 1: return sddmm_ve_side<QH, 1>(a, s);
+        case 2: return sddmm_ve_side<QH, 2>(a, s);
+        default: return sddmm_ve_side<QH, 3>(a, s);
+    }
+}
+
 int tune_sddmm() {
     static int v = [] {
         const char *e = getenv("GSP_TUNE_SDDMM");
@@ -220,8 +284,18 @@ cudaError_t launch_sddmm(const SddmmArgs &a, cudaStream_t s) {
 
 cudaError_t launch_sddmm_ve(const SddmmVeArgs &a, cudaStream_t s) {
     if (a.nrows == 0 || a.H == 0) return cudaSuccess;
-    sddmm_ve_kernel<<<(unsigned)ceil_div(a.nrows, kWarps), kThreads, 0, s>>>(a);
-    return cudaGetLastError();
+    const bool vec = (a.H == 4 || a.H == 8 || a.H == 16 || a.H == 32) && a.ldw % 4 == 0 && a.ldo % 4 == 0 &&
+                     a.ldx % 4 == 0 && aligned(a.w, 16) && aligned(a.out, 16) && aligned(a.X, 16);
+    if (!vec) {
+        sddmm_ve_kernel<<<(unsigned)ceil_div(a.nrows, kWarps), kThreads, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    switch (a.H) {
+        case 4: return sddmm_ve_op<1>(a, s);
+        case 8: return sddmm_ve_op<2>(a, s);
+        case 16: return sddmm_ve_op<4>(a, s);
+        default: return sddmm_ve_op<8>(a, s);
+    }
 }
 
 }  // namespace gsp

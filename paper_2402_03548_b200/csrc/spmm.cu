@@ -322,6 +322,94 @@ __global__ void __launch_bounds__(kThreads) spmm_e_kernel(const SpmmEArgs a) {
     }
 }
 
+// Vector path (H in {4, 8, 16, 32}, 16-B aligned rows): QH = H/4 lanes per edge,
+// one float4 of heads each, EPW = 32/QH edges per warp step, 4 steps in
+// flight; the LPT schedule of the other kernels (heavy rows: one CTA, warps
+// combined in a fixed order through shared memory -> deterministic).
+template <int QH, int RED, bool EID>
+__global__ void __launch_bounds__(kThreads) spmm_e_vec_kernel(const SpmmEArgs a) {
+    constexpr int EPW = 32 / QH, U = 4;
+    __shared__ double part[kWarps][4 * QH];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t row, b, e;
+    bool heavy;
+    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    const Pol pol = make_pol();
+    const int eo = lane / QH, q = lane % QH;
+    auto comb = [](double x, double y) {
+        if constexpr (RED == 1) return y < x ? y : x;
+        else if constexpr (RED == 2) return y > x ? y : x;
+        else return x + y;
+    };
+    constexpr double ID = RED == 1 ? INFINITY : (RED == 2 ? -INFINITY : 0.0);
+    double acc[4] = {ID, ID, ID, ID};
+    const float *wq = a.w + 4 * q;
+    auto addv = [&](const float4 v) {
+        acc[0] = comb(acc[0], (double)v.x); acc[1] = comb(acc[1], (double)v.y);
+        acc[2] = comb(acc[2], (double)v.z); acc[3] = comb(acc[3], (double)v.w);
+    };
+    int64_t j = b + eo;
+    for (; j + (U - 1) * EPW < e; j += U * EPW) {
+        int64_t ei[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) ei[u] = EID ? (int64_t)ld_stream_i32(a.eid + j + u * EPW, pol.stream) : j + u * EPW;
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) v[u] = ld_stream_f4(wq + ei[u] * a.ldw, pol.stream);
+#pragma unroll
+        for (int u = 0; u < U; u++) addv(v[u]);
+    }
+    for (; j < e; j += EPW) {
+        const int64_t ei = EID ? (int64_t)ld_stream_i32(a.eid + j, pol.stream) : j;
+        addv(ld_stream_f4(wq + ei * a.ldw, pol.stream));
+    }
+#pragma unroll
+    for (int o = QH; o < 32; o <<= 1) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) acc[k] = comb(acc[k], __shfl_xor_sync(kFull, acc[k], o));
+    }
+    if (!heavy) {
+        if (eo == 0) {
+            float *o = a.out + row * a.ldo + 4 * q;
+#pragma unroll
+            for (int k = 0; k < 4; k++) o[k] = b == e ? 0.f : (float)acc[k];
+        }
+        return;
+    }
+    if (eo == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) part[warp][4 * q + k] = acc[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 * QH) {
+        double v = ID;
+#pragma unroll
+        for (int w = 0; w < kWarps; w++) v = comb(v, part[w][threadIdx.x]);
+        a.out[row * a.ldo + threadIdx.x] = (float)v;
+    }
+}
+
+template <int QH>
+cudaError_t spmm_e_red(const SpmmEArgs &a, cudaStream_t s) {
+    const dim3 grid = row_grid(a.nrows, a.n_heavy, 1);
+    const bool eid = a.eid != nullptr;
+    switch (a.red) {
+        case 1:
+            if (eid) spmm_e_vec_kernel<QH, 1, true><<<grid, kThreads, 0, s>>>(a);
+            else spmm_e_vec_kernel<QH, 1, false><<<grid, kThreads, 0, s>>>(a);
+            break;
+        case 2:
+            if (eid) spmm_e_vec_kernel<QH, 2, true><<<grid, kThreads, 0, s>>>(a);
+            else spmm_e_vec_kernel<QH, 2, false><<<grid, kThreads, 0, s>>>(a);
+            break;
+        default:
+            if (eid) spmm_e_vec_kernel<QH, 0, true><<<grid, kThreads, 0, s>>>(a);
+            else spmm_e_vec_kernel<QH, 0, false><<<grid, kThreads, 0, s>>>(a);
+            break;
+    }
+    return cudaGetLastError();
+}
+
 __global__ void gather_scale_kernel(const int32_t *col, int64_t nnz, const float *scale, float *out) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x)
         out[j] = scale[col[j]];
@@ -424,8 +512,17 @@ cudaError_t launch_spmm(const SpmmArgs &a, int mode, cudaStream_t s) {
 
 cudaError_t launch_spmm_e(const SpmmEArgs &a, cudaStream_t s) {
     if (a.nrows == 0 || a.H == 0) return cudaSuccess;
-    spmm_e_kernel<<<(unsigned)ceil_div(a.nrows, kWarps), kThreads, 0, s>>>(a);
-    return cudaGetLastError();
+    const bool vec = (a.H == 4 || a.H == 8 || a.H == 16 || a.H == 32) && a.ldw % 4 == 0 && aligned(a.w, 16);
+    if (!vec) {
+        spmm_e_kernel<<<(unsigned)ceil_div(a.nrows, kWarps), kThreads, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    switch (a.H) {
+        case 4: return spmm_e_red<1>(a, s);
+        case 8: return spmm_e_red<2>(a, s);
+        case 16: return spmm_e_red<4>(a, s);
+        default: return spmm_e_red<8>(a, s);
+    }
 }
 
 cudaError_t launch_gather_scale(const int32_t *col, int64_t nnz, const float *scale, float *out, cudaStream_t s) {

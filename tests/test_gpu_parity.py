@@ -471,7 +471,7 @@ def test_gspmm_reduce_minmax(gsp, F, ld):
                     assert np.array_equal(out.astype(np.float64), ref), (red, rev)
 
 
-@pytest.mark.parametrize("H", [1, 2, 8, 5, 40])
+@pytest.mark.parametrize("H", [1, 2, 4, 8, 16, 32, 5, 40])
 def test_gspmm_e(gsp, H):
     for seed in range(2):
         rng = np.random.default_rng(seed + 3 * H)
@@ -491,7 +491,7 @@ def test_gspmm_e(gsp, H):
                     assert np.array_equal(out.astype(np.float64), ref), (red, rev)
 
 
-@pytest.mark.parametrize("H", [1, 3, 8])
+@pytest.mark.parametrize("H", [1, 3, 4, 8, 16, 32])
 def test_gsddmm_ve(gsp, H):
     rng = np.random.default_rng(H)
     V = int(rng.integers(1, 2500))
@@ -513,6 +513,45 @@ def test_gsddmm_ve(gsp, H):
     row_of = np.repeat(np.arange(V), np.diff(og.fwd_off))
     ref = (a_dst[row_of].astype(np.float32) + a_src[og.fwd_col].astype(np.float32))
     assert np.array_equal(e.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("H,ld", [(8, 8), (8, 12), (8, 10), (16, 20), (4, 4)])
+def test_next3_heavy_rows_and_strides(gsp, H, ld):
+    """gSpMMe / gSDDMMve on a graph with CTA-split hub rows (degree 3000 and
+    1025, just past the 1024-edge heavy threshold), empty rows and ragged
+    light rows; edge-value rows padded to ld (NaN padding: never read)."""
+    rng = np.random.default_rng(H * 100 + ld)
+    V = 3100
+    hub_src = rng.integers(0, V, 3000 + 1025)
+    hub_dst = np.concatenate([np.zeros(3000, np.int64), np.full(1025, 7, np.int64)])
+    m = 6000
+    s2, d2 = rng.integers(0, V, m), rng.integers(20, V - 20, m)
+    src = np.concatenate([hub_src, s2]).astype(np.int64)
+    dst = np.concatenate([hub_dst, d2]).astype(np.int64)
+    E = len(src)
+    G, og = graph_pair(gsp, V, src, dst)
+    wh = datagen.uniform(H + ld, E, H)
+    w = padded(wh, ld)
+    for red in (gsp.REDUCE_SUM, gsp.REDUCE_MIN, gsp.REDUCE_MAX):
+        for rev in (0, 1):
+            ref, T = og.gspmm_e(wh, red, bool(rev))
+            out = G.gspmm_e(w, red, reverse=rev).cpu().numpy()
+            if red == gsp.REDUCE_SUM:
+                assert_within(out, ref, T, f"gspmm_e sum r{rev}")
+            else:
+                assert np.array_equal(out.astype(np.float64), ref), (red, rev)
+    Xh = datagen.uniform(9, V, H, lo=0.5, hi=2.0)
+    X = padded(Xh, ld)
+    for op in (gsp.OP_ADD, gsp.OP_SUB, gsp.OP_MUL, gsp.OP_DIV):
+        for side in (gsp.SIDE_DST, gsp.SIDE_SRC):
+            ref = og.gsddmm_ve(Xh, wh, op, side).astype(np.float32)
+            out = padded(np.zeros((E, H), np.float32), ld)
+            G.gsddmm_ve(X, w, op, side, out=out)
+            assert np.array_equal(out.cpu().numpy(), ref), (op, side)
+            # in place: out aliases w
+            w2 = padded(wh, ld)
+            G.gsddmm_ve(X, w2, op, side, out=w2)
+            assert np.array_equal(w2.cpu().numpy(), ref), (op, side, "in place")
 
 
 # ------------------------------------------------ tile / bin boundary degrees

@@ -27,6 +27,7 @@ out = torch.empty((V, F), device="cuda")
 outg = torch.empty((V, Fg), device="cuda")
 s = torch.empty((E, H), device="cuda")
 s2 = torch.rand((E, H), device="cuda")
+outh = torch.empty((V, H), device="cuda")
 flush = torch.empty(512 << 18, device="cuda")
 ops = {
     "gspmm_fwd": lambda: G.gspmm(X, 2, out=out),
@@ -40,6 +41,10 @@ ops = {
     "wrev": lambda: G.gspmm_weighted(Z, s, out=outg, reverse=True),
     "gat_fused": lambda: G.gat_forward(Z, Z, Z, H, alpha=s, out=outg),
     "softmax_bwd": lambda: G.edge_softmax_backward(s, s2, out=s2),
+    "e_sum": lambda: G.gspmm_e(s, 0, out=outh),
+    "e_sum_rev": lambda: G.gspmm_e(s, 0, out=outh, reverse=True),
+    "ve_src": lambda: G.gsddmm_ve(Z[:, :H], s2, 0, 1, out=s),
+    "ve_dst": lambda: G.gsddmm_ve(Z[:, :H], s2, 0, 0, out=s),
 }
 G.gsddmm(Z, Z, out=s); G.edge_softmax(s, out=s)
 res = {}
