@@ -44,7 +44,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with tempfile.TemporaryDirectory(prefix="gsp_build_") as tmpdir:
         def compile_one(src):
             obj = os.path.join(tmpdir, os.path.basename(src) + ".o")
-            cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
+            extra = os.environ.get("GSP_NVCC_EXTRA", "").split()   # experiments only (e.g. -D knobs)
+            cmd = ["nvcc", *NVCC_FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             r = subprocess.run(cmd, capture_output=True, text=True)

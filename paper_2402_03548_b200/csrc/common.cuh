@@ -106,6 +106,15 @@ __device__ __forceinline__ float4 ld_stream_f4(const float *p, uint64_t pol) {
     return v;
 }
 
+// bulk L2 prefetch of the 16-B-aligned span covering [p, p + bytes) (a hint:
+// streamed edge arrays reach L2 tiles ahead of their register loads).  The span
+// may round past the array end by < 16 B: device allocations are >= 256-B granular.
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+    const uintptr_t s = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s), "r"((uint32_t)(e - s)) : "memory");
+}
+
 // async global -> shared copies (LDGSTS): edge-value rows land in smem without
 // occupying registers; src_size 0 zero-fills (padding lanes)
 __device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, int src_size) {

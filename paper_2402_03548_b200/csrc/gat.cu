@@ -24,7 +24,8 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
     // running Kahan state (acc, accc) per lane lives in smem: touched once per
     // tile (fold) and on the rare max increase (rescale), keeping registers for
     // the gathers in flight.  Reused for the heavy-row cross-warp merge.
-    __shared__ __align__(16) float s_run[kWarps][32][2 * VEC];
+    // [t][lane]: lane-minor, so the per-lane accesses are bank-conflict free
+    __shared__ __align__(16) float s_run[kWarps][2 * VEC][32];
     __shared__ float sm_ms[kWarps][LPE][2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / LPE, h = lane % LPE;   // head of this lane
@@ -43,9 +44,9 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
 
     // (m, S + Sc compensation) in registers; acc / accc in smem; tile sums in registers
     float m = -INFINITY, S = 0.f, Sc = 0.f, St = 0.f;
-    float *run = s_run[warp][lane];
+    auto run = [&](int t) -> float & { return s_run[warp][t][lane]; };
 #pragma unroll
-    for (int t = 0; t < 2 * VEC; t++) run[t] = 0.f;
+    for (int t = 0; t < 2 * VEC; t++) run(t) = 0.f;
     Vec<VEC> acct;
     vzero(acct);
     int ntile = 0;
@@ -114,8 +115,8 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
                 S *= r; Sc *= r; St *= r;
 #pragma unroll
                 for (int t = 0; t < VEC; t++) {
-                    run[t] *= r;
-                    run[VEC + t] *= r;
+                    run(t) *= r;
+                    run(VEC + t) *= r;
                     acct.v[t] *= r;
                 }
                 m = mb;
@@ -143,11 +144,11 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
             Sc = (t2 - S) - y2; S = t2; St = 0.f;
 #pragma unroll
             for (int t = 0; t < VEC; t++) {
-                const float ac = run[t], cc = run[VEC + t];
+                const float ac = run(t), cc = run(VEC + t);
                 y2 = acct.v[t] - cc;
                 t2 = ac + y2;
-                run[VEC + t] = (t2 - ac) - y2;
-                run[t] = t2;
+                run(VEC + t) = (t2 - ac) - y2;
+                run(t) = t2;
                 acct.v[t] = 0.f;
             }
         }
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
     S -= Sc;
     Vec<VEC> acc;
 #pragma unroll
-    for (int t = 0; t < VEC; t++) acc.v[t] = run[t] - run[VEC + t];
+    for (int t = 0; t < VEC; t++) acc.v[t] = run(t) - run(VEC + t);
     // merge the G edge groups (same head h): online-softmax merge
     auto merge = [&](float mo, float So, const Vec<VEC> &ao) {
         const float mn = fmaxf(m, mo);
@@ -177,11 +178,12 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
     if (heavy) {
         // every warp of the CTA holds (m, S, acc) of its slice per head: merge in warp order
         __syncthreads();   // s_run is reused for the cross-warp state
+        float *xs = &s_run[0][0][0];   // [warp][head][t] scratch
         if (g == 0) {
             sm_ms[warp][h][0] = m;
             sm_ms[warp][h][1] = S;
 #pragma unroll
-            for (int t = 0; t < VEC; t++) s_run[warp][h][t] = acc.v[t];
+            for (int t = 0; t < VEC; t++) xs[(warp * 32 + h) * VEC + t] = acc.v[t];
         }
         __syncthreads();
         m = -INFINITY;
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
         for (int w = 0; w < kWarps; w++) {
             Vec<VEC> ao;
 #pragma unroll
-            for (int t = 0; t < VEC; t++) ao.v[t] = s_run[w][h][t];
+            for (int t = 0; t < VEC; t++) ao.v[t] = xs[(w * 32 + h) * VEC + t];
             merge(sm_ms[w][h][0], sm_ms[w][h][1], ao);
         }
     }

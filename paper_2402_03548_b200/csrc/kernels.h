@@ -24,6 +24,7 @@ struct SpmmArgs {
     const float *w;          // weighted modes
     int64_t ldw;
     int64_t H, Fh;
+    int pf;                  // L2 prefetch distance of the edge streams, in 32-edge tiles (0 = off)
 };
 
 enum SpmmMode { kSpmmScaled = 0, kSpmmWeightedFwd = 1, kSpmmWeightedRev = 2, kSpmmMin = 3, kSpmmMax = 4 };

@@ -1,6 +1,10 @@
 // gSpMM family: gSpMMv + norm, gSpMMve / gSpMMve^T, min / max, gSpMMe (+ degree / edge scales).
 #include "common.cuh"
 
+#ifndef GSP_PAIR_LAYOUT
+#define GSP_PAIR_LAYOUT 1
+#endif
+
 namespace gsp {
 namespace {
 
@@ -25,13 +29,18 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
         else return x + y;
     };
     constexpr int RED = kWarps * SW;
-    constexpr int WS = W ? 2 * kWarps * 32 * kHMax : 0;   // double-buffered weight rows
+    // double-buffered weight rows; each edge group's rows start 8 words (one
+    // bank octet) after the previous group's, so the 32/LPE groups of a warp
+    // read their per-edge weights from distinct banks (no 4-way conflicts)
+    constexpr int WP = G <= 4 ? 8 : 4;   // group padding (words, keeps 16-B rows); narrower for many groups (48 KB static smem)
+    constexpr int WSW = 32 * kHMax + WP * G;
+    constexpr int WS = W ? 2 * kWarps * WSW : 0;
     __shared__ __align__(16) int2 s_pair[kWarps][32];
     __shared__ __align__(16) float s_raw[RED > WS ? RED : WS];   // weights during the walk, then heavy combine
     // Kahan compensation of narrow lanes lives in smem (touched once per fold):
     // the registers go to gathers in flight
     constexpr bool CMP_SMEM = VEC * CPL <= 8 && !MM;
-    __shared__ __align__(16) float s_cmp[CMP_SMEM ? kWarps : 1][CMP_SMEM ? 32 : 1][CMP_SMEM ? VEC * CPL : 1];
+    __shared__ __align__(16) float s_cmp[CMP_SMEM ? kWarps : 1][CMP_SMEM ? VEC * CPL : 1][CMP_SMEM ? 32 : 1];   // lane-minor: conflict-free
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / LPE, sub = lane % LPE;
@@ -69,7 +78,7 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     constexpr int NT = VEC >= 4 ? 1 : 2;   // independent tile accumulators (ILP for narrow lanes)
     Vec<VEC> acc[CPL], cmp_r[CMP_SMEM ? 1 : CPL], tile[NT][CPL];
     auto cmp_ref = [&](int q, int t) -> float & {
-        if constexpr (CMP_SMEM) return s_cmp[warp][lane][q * VEC + t];
+        if constexpr (CMP_SMEM) return s_cmp[warp][q * VEC + t][lane];
         else return cmp_r[q].v[t];
     };
 #pragma unroll
@@ -89,7 +98,15 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     // loaded two tiles ahead, the dependent per-edge scale one tile ahead, and
     // weight rows are copied global -> smem asynchronously one tile ahead
     // (double buffer), so a tile's gathers never wait on its own index trips.
-    const int slot = (lane % G) * PER + lane / G;   // group-contiguous layout
+    const int wpos = (lane % G) * (PER * H + WP) + (lane / G) * H;   // this lane's weight row in s_w
+    // (col, scale) pairs of group g's edges i, i+1 (i even) sit in one 16-B
+    // chunk, the G groups' chunks side by side: one LDS.128 per two edges reads
+    // 16*G contiguous bytes, conflict-free
+#if GSP_PAIR_LAYOUT == 0
+    const int ppos = (lane % G) * PER + lane / G;
+#else
+    const int ppos = ((lane / G) >> 1) * 2 * G + 2 * (lane % G) + ((lane / G) & 1);
+#endif
     auto load_idx = [&](int64_t tb, int &c, int &ev) {
         c = 0;
         ev = 0;
@@ -121,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     auto issue_w = [&](int64_t tb, int ev, int buf) {
         if constexpr (W) {
             if (w8) return;
-            float *dst = s_raw + (buf * kWarps + warp) * 32 * kHMax + slot * H;
+            float *dst = s_raw + (buf * kWarps + warp) * WSW + wpos;
             const bool valid = tb + lane < e;
             const float *src = a.w + (int64_t)(valid ? ev : 0) * a.ldw;
             if (w16) {
@@ -132,6 +149,19 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
             cp_async_commit();
         }
     };
+    // L2 prefetch of the streamed edge arrays a.pf tiles ahead (lane 0, one
+    // bulk request per stream and tile)
+    const bool pfw = MODE == kSpmmWeightedFwd && (a.ldw % 4 == 0);
+    auto prefetch = [&](int64_t tb, int64_t n) {
+        if (lane != 0 || tb >= e) return;
+        n = n < e - tb ? n : e - tb;
+        prefetch_l2(a.col + tb, (uint32_t)(n * 4));
+        if constexpr (MODE == kSpmmScaled)
+            if (a.edge_scale) prefetch_l2(a.edge_scale + tb, (uint32_t)(n * 4));
+        if constexpr (MODE == kSpmmWeightedRev) prefetch_l2(a.eid + tb, (uint32_t)(n * 4));
+        if (pfw) prefetch_l2(a.w + tb * a.ldw, (uint32_t)(n * a.ldw * 4));
+    };
+    if (a.pf) prefetch(b, (int64_t)a.pf * 32);
     int c1, e1, c2, e2;
     load_idx(b, c1, e1);
     load_idx(b + 32, c2, e2);
@@ -143,7 +173,8 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
 
     for (int64_t base = b; base < e; base += 32) {
         const int n = (int)(e - base < 32 ? e - base : 32);
-        s_pair[warp][slot] = make_int2(c1, __float_as_int(wv1));
+        if (a.pf) prefetch(base + (int64_t)a.pf * 32, 32);
+        s_pair[warp][ppos] = make_int2(c1, __float_as_int(wv1));
         // ---- advance the pipeline before this tile's gathers
         int c3, e3;
         load_idx(base + 64, c3, e3);
@@ -151,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
         float w8b[W ? 8 : 1];
         if constexpr (W) {
             if (w8) {
-                float *dst = s_raw + (buf * kWarps + warp) * 32 * kHMax + slot * 8;
+                float *dst = s_raw + (buf * kWarps + warp) * WSW + wpos;
                 reinterpret_cast<float4 *>(dst)[0] = make_float4(w8a[0], w8a[1], w8a[2], w8a[3]);
                 reinterpret_cast<float4 *>(dst)[1] = make_float4(w8a[4], w8a[5], w8a[6], w8a[7]);
                 load_w8(base + 32, e2, w8b);
@@ -160,17 +191,25 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
                 cp_async_wait<1>();   // this tile's weight rows have landed
             }
         }
-        const float *s_w = s_raw + (buf * kWarps + warp) * 32 * kHMax;
+        const float *s_w = s_raw + (buf * kWarps + warp) * WSW;
         __syncwarp();
+#if GSP_PAIR_LAYOUT == 0
         const int2 *gp = &s_pair[warp][g * PER];
-        const float *gw = s_w + g * PER * H;
+#else
+        const int2 *gp = &s_pair[warp][2 * g];
+#endif
+        const float *gw = s_w + g * (PER * H + WP);
 
         auto body = [&](int i, bool full, int m) {
             Vec<VEC> x[U][CPL];
             float wt[U][CPL];
 #pragma unroll
             for (int u = 0; u < U; u += 2) {
+#if GSP_PAIR_LAYOUT == 0
                 const int4 pp = *reinterpret_cast<const int4 *>(gp + i + u);
+#else
+                const int4 pp = *reinterpret_cast<const int4 *>(gp + (i + u) * G);
+#endif
                 const int cc[2] = {pp.x, pp.z};
                 const float ww[2] = {__int_as_float(pp.y), __int_as_float(pp.w)};
 #pragma unroll
@@ -497,8 +536,18 @@ cudaError_t spmm_dispatch(const SpmmArgs &a, int mode, cudaStream_t s) {
 
 }  // namespace
 
-cudaError_t launch_spmm(const SpmmArgs &a, int mode, cudaStream_t s) {
-    if (a.nrows == 0 || a.F == 0) return cudaSuccess;
+static int prefetch_tiles() {
+    static int v = [] {
+        const char *e = getenv("GSP_PF");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
+cudaError_t launch_spmm(const SpmmArgs &a_in, int mode, cudaStream_t s) {
+    if (a_in.nrows == 0 || a_in.F == 0) return cudaSuccess;
+    SpmmArgs a = a_in;
+    a.pf = prefetch_tiles();
     const bool wmode = mode == kSpmmWeightedFwd || mode == kSpmmWeightedRev;
     if (wmode && a.H > kHMax) return cudaErrorNotSupported;   // api.cu rejects H > 16 first
     auto ok_vec = [&](int v) {
