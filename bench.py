@@ -512,12 +512,13 @@ def main_gsp(args):
     # ------------------------------------------- NEXT rows (outside the step)
     next_rows = None
     if not args.profile:
-        def time_op(fn, reps=5):
+        def time_op(fn, reps=5, flush_l2=True):
             for _ in range(2):
                 fn()
             ts = []
             for _ in range(reps):
-                flush.fill_(1.0)
+                if flush_l2:
+                    flush.fill_(1.0)
                 a0 = torch.cuda.Event(enable_timing=True)
                 a1 = torch.cuda.Event(enable_timing=True)
                 a0.record(stream)
@@ -553,6 +554,23 @@ def main_gsp(args):
                                       "GB_s": round(alg_bytes("edge_softmax", Vloc, Eloc, F, H) * 1.5 / (ms_sbw * 1e-3) / 1e9, 1)},
         }
         del alpha2, gout, dal, hout
+        # context: warm-L2 times of the headline op (no flush:
+        # steady state layer to layer) and the paper's kernel-plot shapes
+        # (F = 32, one head: P:2308) on the same graph
+        warm_ms = time_op(lambda: part.gspmm(X, gsp.NORM_BOTH, out=outs[0], stream=stream), flush_l2=False)
+        X32 = torch.rand((part.ncols, 32), device="cuda") - 0.5
+        w1 = torch.rand((Ep, 1), device="cuda")
+        o32 = torch.empty((R, 32), device="cuda")
+        shapes = {
+            "gspmm_fwd_F32": time_op(lambda: part.gspmm(X32, gsp.NORM_BOTH, out=o32, stream=stream)),
+            "gspmm_weighted_rev_F32_H1": time_op(lambda: part.gspmm_weighted(X32, w1, out=o32, reverse=True,
+                                                                             stream=stream)) if P == 1 else None,
+            "gsddmm_F32_H1": time_op(lambda: part.gsddmm(X32, X32, H=1, out=w1, stream=stream)),
+        }
+        next_rows["context"] = {"gspmm_fwd_warm_l2_ms": round(warm_ms, 4),
+                                "paper_plot_shapes_ms": {k: (round(v, 4) if v is not None else None)
+                                                         for k, v in shapes.items()}}
+        del X32, w1, o32
 
     per_op = {}
     bytes_of = {"gspmm_fwd": alg_bytes("gspmm", Vloc, Eloc, F, H), "gspmm_rev": alg_bytes("gspmm", Vloc, Eloc, F, H),

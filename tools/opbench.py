@@ -14,6 +14,14 @@ ap.add_argument("--ld", type=int, default=0)
 ap.add_argument("--tag", default=os.environ.get("GSP_TUNE_SPMM", ""))
 args = ap.parse_args()
 cfg = datagen.CONFIGS[args.config]
+if os.environ.get("GSP_PERSIST_MB"):   # experiment: L2 set-aside for persisting (evict_last) lines
+    import ctypes
+    torch.cuda.init(); torch.empty(1, device="cuda")
+    rt = ctypes.CDLL(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime", "lib", "libcudart.so.12"))
+    mb = int(os.environ["GSP_PERSIST_MB"])
+    st = rt.cudaDeviceSetLimit(6, ctypes.c_size_t(mb << 20))
+    got = ctypes.c_size_t(0); rt.cudaDeviceGetLimit(ctypes.byref(got), 6)
+    print("persist limit", st, got.value >> 20, "MB", file=sys.stderr)
 V, src, dst = datagen.make_graph(cfg)
 G = gsp.Graph(V, src, dst, device=0)
 E = G.E
