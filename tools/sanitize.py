@@ -21,6 +21,20 @@ def run(V, src, dst, F=64, H=8):
     g.gspmm_e(s, 0)
     g.gspmm_e(s, 2, reverse=True)
     g.gsddmm_ve(X[:, :H], s, 0, 1)
+    for red in (0, 1, 2):                      # vector gSpMMe paths (H = 4, 8, 16; fwd + rev)
+        for hh in (4, 16):
+            w = torch.rand((g.E, hh), device="cuda")
+            g.gspmm_e(w, red)
+            g.gspmm_e(w, red, reverse=True)
+        g.gspmm_e(s, red)
+    for op in range(4):                        # vector gSDDMMve, both sides, in place
+        for side in (0, 1):
+            g.gsddmm_ve(X[:, :H], s, op, side)
+            t = s.clone()
+            g.gsddmm_ve(X[:, :H], t, op, side, out=t)
+    wp = torch.rand((g.E, 12), device="cuda")[:, :8]   # padded rows (ld 12)
+    g.gspmm_e(wp, 0)
+    g.gsddmm_ve(X[:, :8], wp, 0, 1, out=wp)
     # odd shapes (generic / scalar paths)
     X3 = torch.from_numpy(datagen.uniform(2, V, 15)).cuda()
     g.gspmm(X3, 2)
