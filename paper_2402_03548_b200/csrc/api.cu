@@ -116,13 +116,23 @@ gsp_status upload_structure(gsp_graph *g, gsp::DevStructure &S, int64_t nrows, i
         if ((st = dev_upload(g, col.data(), col.size(), &S.col)) != GSP_OK) return st;
     }
     if (eid && (st = dev_upload(g, eid->data(), eid->size(), &S.eid)) != GSP_OK) return st;
-    if (shared_order) {
+    if (shared_order) {   // same offsets (symmetric topology): same schedule
         S.order = shared_order;
+        S.task = share_topology->task;
         S.n_heavy = shared_n_heavy;
     } else {
         std::vector<int32_t> order;
         gsp::degree_order(off.data(), nrows, gsp::kHeavyThreshold, order, S.n_heavy);
         if ((st = dev_upload(g, order.data(), order.size(), &S.order)) != GSP_OK) return st;
+        std::vector<int32_t> task((size_t)nrows * 4);
+        for (int64_t i = 0; i < nrows; i++) {
+            const int64_t r = order[i], b = off[r];
+            task[4 * i] = (int32_t)r;
+            task[4 * i + 1] = (int32_t)(off[r + 1] - b);   // degree < 2^31 (E < 2^31)
+            task[4 * i + 2] = (int32_t)(uint32_t)((uint64_t)b & 0xffffffffu);
+            task[4 * i + 3] = (int32_t)(uint32_t)((uint64_t)b >> 32);
+        }
+        if ((st = dev_upload(g, task.data(), task.size(), &S.task)) != GSP_OK) return st;
     }
     return GSP_OK;
 }
@@ -372,7 +382,7 @@ gsp_status gsp_gspmm(const gsp_graph *g, const gsp_tensor *X, int norm, gsp_tens
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SpmmArgs a{};
-    a.off = S.off; a.col = S.col; a.eid = nullptr; a.order = S.order;
+    a.off = S.off; a.col = S.col; a.eid = nullptr; a.order = S.order; a.task = S.task;
     a.nrows = S.nrows; a.n_heavy = S.n_heavy;
     a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
     a.out = static_cast<float *>(out->data); a.ldo = out->ld;
@@ -406,7 +416,7 @@ gsp_status gsp_gspmm_weighted(const gsp_graph *g, const gsp_tensor *X, const gsp
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SpmmArgs a{};
-    a.off = S.off; a.col = S.col; a.eid = S.eid; a.order = S.order;
+    a.off = S.off; a.col = S.col; a.eid = S.eid; a.order = S.order; a.task = S.task;
     a.nrows = S.nrows; a.n_heavy = S.n_heavy;
     a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
     a.out = static_cast<float *>(out->data); a.ldo = out->ld;
@@ -435,7 +445,7 @@ gsp_status gsp_gsddmm(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor 
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SddmmArgs a{};
-    a.off = S.off; a.col = S.col; a.order = S.order;
+    a.off = S.off; a.col = S.col; a.order = S.order; a.task = S.task;
     a.nrows = S.nrows; a.n_heavy = S.n_heavy; a.row_base = g->row_base;
     a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
     a.Y = static_cast<const float *>(Y->data); a.ldy = Y->ld;
@@ -466,7 +476,7 @@ gsp_status gsp_edge_softmax(const gsp_graph *g, const gsp_tensor *e_in, gsp_tens
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SoftmaxArgs a{};
-    a.off = S.off; a.order = S.order; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.off = S.off; a.order = S.order; a.task = S.task; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
     a.e = static_cast<const float *>(e_in->data); a.lde = e_in->ld;
     a.out = static_cast<float *>(out->data); a.ldo = out->ld;
     a.H = e_in->cols;
@@ -491,7 +501,7 @@ gsp_status gsp_edge_softmax_backward(const gsp_graph *g, const gsp_tensor *alpha
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SoftmaxBwdArgs a{};
-    a.off = S.off; a.order = S.order; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.off = S.off; a.order = S.order; a.task = S.task; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
     a.alpha = static_cast<const float *>(alpha->data); a.lda = alpha->ld;
     a.dalpha = static_cast<const float *>(dalpha->data); a.ldd = dalpha->ld;
     a.out = static_cast<float *>(dscore->data); a.ldo = dscore->ld;
@@ -524,7 +534,7 @@ gsp_status gsp_gat_forward(const gsp_graph *g, const gsp_tensor *X, const gsp_te
     DeviceGuard dg(g->device);
     cudaStream_t cs = (cudaStream_t)stream;
     gsp::GatArgs ga{};
-    ga.off = S.off; ga.col = S.col; ga.order = S.order; ga.nrows = S.nrows; ga.n_heavy = S.n_heavy;
+    ga.off = S.off; ga.col = S.col; ga.order = S.order; ga.task = S.task; ga.nrows = S.nrows; ga.n_heavy = S.n_heavy;
     ga.row_base = g->row_base;
     ga.X = static_cast<const float *>(X->data); ga.ldx = X->ld;
     ga.Y = static_cast<const float *>(Y->data); ga.ldy = Y->ld;
@@ -539,7 +549,7 @@ gsp_status gsp_gat_forward(const gsp_graph *g, const gsp_tensor *X, const gsp_te
     } else {
         // any other shape: the three kernels in sequence (same results within the bound)
         gsp::SddmmArgs sa{};
-        sa.off = S.off; sa.col = S.col; sa.order = S.order; sa.nrows = S.nrows; sa.n_heavy = S.n_heavy;
+        sa.off = S.off; sa.col = S.col; sa.order = S.order; sa.task = S.task; sa.nrows = S.nrows; sa.n_heavy = S.n_heavy;
         sa.row_base = g->row_base;
         sa.X = ga.X; sa.ldx = X->ld; sa.Y = ga.Y; sa.ldy = Y->ld;
         sa.out = ga.alpha; sa.ldo = alpha->ld; sa.H = H; sa.Fh = X->cols / H;
@@ -547,13 +557,13 @@ gsp_status gsp_gat_forward(const gsp_graph *g, const gsp_tensor *X, const gsp_te
                       : cudaMemset2DAsync(alpha->data, (size_t)alpha->ld * 4, 0, (size_t)H * 4, (size_t)g->E, cs);
         if (e == cudaSuccess) {
             gsp::SoftmaxArgs xa{};
-            xa.off = S.off; xa.order = S.order; xa.nrows = S.nrows; xa.n_heavy = S.n_heavy;
+            xa.off = S.off; xa.order = S.order; xa.task = S.task; xa.nrows = S.nrows; xa.n_heavy = S.n_heavy;
             xa.e = ga.alpha; xa.lde = alpha->ld; xa.out = ga.alpha; xa.ldo = alpha->ld; xa.H = H;
             e = gsp::launch_softmax(xa, cs);
         }
         if (e == cudaSuccess) {
             gsp::SpmmArgs wa{};
-            wa.off = S.off; wa.col = S.col; wa.order = S.order; wa.nrows = S.nrows; wa.n_heavy = S.n_heavy;
+            wa.off = S.off; wa.col = S.col; wa.order = S.order; wa.task = S.task; wa.nrows = S.nrows; wa.n_heavy = S.n_heavy;
             wa.X = ga.Vt; wa.ldx = Vt->ld; wa.out = ga.out; wa.ldo = out->ld; wa.F = Vt->cols;
             wa.w = ga.alpha; wa.ldw = alpha->ld; wa.H = H; wa.Fh = Vt->cols / H > 0 ? Vt->cols / H : 1;
             e = gsp::launch_spmm(wa, gsp::kSpmmWeightedFwd, cs);
@@ -582,7 +592,7 @@ gsp_status gsp_gspmm_reduce(const gsp_graph *g, const gsp_tensor *X, int reduce,
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SpmmArgs a{};
-    a.off = S.off; a.col = S.col; a.order = S.order; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.off = S.off; a.col = S.col; a.order = S.order; a.task = S.task; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
     a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
     a.out = static_cast<float *>(out->data); a.ldo = out->ld;
     a.F = X->cols; a.H = 1; a.Fh = X->cols > 0 ? X->cols : 1;
@@ -608,7 +618,7 @@ gsp_status gsp_gspmm_e(const gsp_graph *g, const gsp_tensor *w, int reduce, gsp_
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SpmmEArgs a{};
-    a.off = S.off; a.eid = reverse ? S.eid : nullptr; a.order = S.order; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.off = S.off; a.eid = reverse ? S.eid : nullptr; a.order = S.order; a.task = S.task; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
     a.w = static_cast<const float *>(w->data); a.ldw = w->ld;
     a.out = static_cast<float *>(out->data); a.ldo = out->ld;
     a.H = w->cols; a.red = reduce;
@@ -635,7 +645,7 @@ gsp_status gsp_gsddmm_ve(const gsp_graph *g, const gsp_tensor *X, const gsp_tens
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SddmmVeArgs a{};
-    a.off = S.off; a.col = S.col; a.order = S.order; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.off = S.off; a.col = S.col; a.order = S.order; a.task = S.task; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
     a.row_base = g->row_base;
     a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
     a.w = static_cast<const float *>(w->data); a.ldw = w->ld;

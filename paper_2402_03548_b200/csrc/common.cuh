@@ -173,24 +173,23 @@ __device__ __forceinline__ void vstore(float *p, const Vec<VEC> &r, int64_t lim)
 
 // Row and edge range of this warp.  Heavy rows: the whole CTA, contiguous
 // 32-aligned slices per warp.  Returns false if the warp has no row.
-__device__ __forceinline__ bool warp_task(const int64_t *off, const int32_t *order, int64_t nrows,
-                                          int64_t n_heavy, int warp, int64_t &row, int64_t &b,
-                                          int64_t &e, bool &heavy) {
+__device__ __forceinline__ bool warp_task(const int32_t *task, int64_t nrows, int64_t n_heavy, int warp,
+                                          int64_t &row, int64_t &b, int64_t &e, bool &heavy) {
     heavy = (int64_t)blockIdx.x < n_heavy;
+    const int64_t idx = heavy ? (int64_t)blockIdx.x : n_heavy + ((int64_t)blockIdx.x - n_heavy) * kWarps + warp;
+    if (idx >= nrows) return false;
+    const int4 t = __ldg(reinterpret_cast<const int4 *>(task) + idx);   // {row, degree, b lo, b hi}
+    row = t.x;
+    const int64_t rb = (int64_t)(((uint64_t)(uint32_t)t.w << 32) | (uint32_t)t.z), deg = t.y;
     if (heavy) {
-        row = order[blockIdx.x];
-        const int64_t rb = off[row], re = off[row + 1];
-        const int64_t deg = re - rb;
+        const int64_t re = rb + deg;
         const int64_t per = (((deg + kWarps - 1) / kWarps) + 31) & ~int64_t(31);
         b = min(re, rb + per * warp);
         e = min(re, b + per);
-        return true;
+    } else {
+        b = rb;
+        e = rb + deg;
     }
-    const int64_t idx = n_heavy + ((int64_t)blockIdx.x - n_heavy) * kWarps + warp;
-    if (idx >= nrows) return false;
-    row = order[idx];
-    b = off[row];
-    e = off[row + 1];
     return true;
 }
 

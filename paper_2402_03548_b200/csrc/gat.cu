@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
 
     int64_t row, b, e;
     bool heavy;
-    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     const Pol pol = make_pol();
 
     Vec<VEC> xv;

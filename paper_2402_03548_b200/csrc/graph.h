@@ -48,6 +48,9 @@ struct DevStructure {
     // degree-binned schedule: rows by descending degree; the first n_heavy
     // rows get a whole CTA each, the rest one warp each.
     const int32_t *order = nullptr;
+    // the same schedule as 16-B records {row, degree, off[row] lo, hi}: one
+    // vector load gives a warp its whole task (no order -> off round trip)
+    const int32_t *task = nullptr;
     int64_t n_heavy = 0;
     int64_t max_deg = 0;
     bool present = false;

@@ -12,6 +12,7 @@ struct SpmmArgs {
     const int32_t *col;
     const int32_t *eid;      // MODE weighted-rev: explicit edge IDs; else unused
     const int32_t *order;    // degree-ordered rows
+    const int32_t *task;     // per schedule slot {row, degree, first slot lo, hi} (16 B; DevStructure::task)
     int64_t nrows, n_heavy;
     const float *X;
     int64_t ldx;
@@ -35,6 +36,7 @@ struct SddmmArgs {
     const int64_t *off;
     const int32_t *col;
     const int32_t *order;
+    const int32_t *task;
     int64_t nrows, n_heavy;
     int64_t row_base;        // X row of local row r is row_base + r
     const float *X;
@@ -50,6 +52,7 @@ cudaError_t launch_sddmm(const SddmmArgs &a, cudaStream_t s);
 struct SoftmaxArgs {
     const int64_t *off;
     const int32_t *order;
+    const int32_t *task;
     int64_t nrows, n_heavy;
     const float *e;
     int64_t lde;
@@ -63,6 +66,7 @@ cudaError_t launch_softmax(const SoftmaxArgs &a, cudaStream_t s);
 struct SoftmaxBwdArgs {
     const int64_t *off;
     const int32_t *order;
+    const int32_t *task;
     int64_t nrows, n_heavy;
     const float *alpha;
     int64_t lda;
@@ -81,6 +85,7 @@ struct GatArgs {
     const int64_t *off;
     const int32_t *col;
     const int32_t *order;
+    const int32_t *task;
     int64_t nrows, n_heavy, row_base;
     const float *X;
     int64_t ldx;
@@ -101,6 +106,7 @@ struct SpmmEArgs {
     const int64_t *off;
     const int32_t *eid;      // null: implicit (slot = edge id)
     const int32_t *order;
+    const int32_t *task;
     int64_t nrows, n_heavy;  // rows in LPT order; the first n_heavy get a CTA each
     const float *w;
     int64_t ldw;
@@ -115,6 +121,7 @@ struct SddmmVeArgs {
     const int64_t *off;
     const int32_t *col;
     const int32_t *order;
+    const int32_t *task;
     int64_t nrows, n_heavy, row_base;
     const float *X;
     int64_t ldx;

@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
 
     int64_t row, b, e;
     bool heavy;
-    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     if (b >= e) return;
     const Pol pol = make_pol();
 
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kThreads) sddmm_generic_kernel(const SddmmArgs
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t row, b, e;
     bool heavy;
-    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     const float *xr = a.X + (a.row_base + row) * a.ldx;
     const int64_t tot = (e - b) * a.H;
     for (int64_t t = lane; t < tot; t += 32) {
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads) sddmm_ve_vec_kernel(const SddmmVeArg
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t row, b, e;
     bool heavy;
-    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     const Pol pol = make_pol();
     const int eo = lane / QH, q = lane % QH;
     float4 xd = make_float4(0.f, 0.f, 0.f, 0.f);

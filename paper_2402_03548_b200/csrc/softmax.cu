@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(kThreads) softmax_kernel(const SoftmaxArgs a) 
     const int HPL = H / VEC > 0 ? H / VEC : 1;
     int64_t row, b, e;
     bool heavy;
-    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     const Pol pol = make_pol();
 
     float m[VEC], s[VEC];
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kThreads) softmax_generic_kernel(const Softmax
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t row, b, e;
     bool heavy;
-    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     for (int64_t h = lane; h < a.H; h += 32) {
         float m = -INFINITY, s = 0.f;
         for (int64_t j = b; j < e; j++) online_push(m, s, a.e[j * a.lde + h]);
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const SoftmaxBwdA
     const int H = (int)a.H, HPL = H / 4;
     int64_t row, b, e;
     bool heavy;
-    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     const Pol pol = make_pol();
     const int64_t lo = b * H, hi = e * H;
     float d[4] = {0.f, 0.f, 0.f, 0.f};
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_generic_kernel(const Sof
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t row, b, e;
     bool heavy;
-    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     for (int64_t h = lane; h < a.H; h += 32) {
         float d = 0.f;
         for (int64_t j = b; j < e; j++) d = fmaf(a.alpha[j * a.lda + h], a.dalpha[j * a.ldd + h], d);

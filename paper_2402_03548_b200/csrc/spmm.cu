@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
 
     int64_t row, b, e;
     bool heavy;
-    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     const Pol pol = make_pol();
     float rs = 1.f;   // row scale, fetched up front (its latency hides under the row's gathers)
     if constexpr (MODE == kSpmmScaled)
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kThreads) spmm_e_vec_kernel(const SpmmEArgs a)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int64_t row, b, e;
     bool heavy;
-    if (!warp_task(a.off, a.order, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     const Pol pol = make_pol();
     const int eo = lane / QH, q = lane % QH;
     auto comb = [](double x, double y) {
