@@ -18,8 +18,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def gsp():
-    from paper_2402_03548_b200 import _build
-    _build.build()
+    from conftest import build_lib
+    build_lib()
     import paper_2402_03548_b200 as m
     return m
 
