@@ -10,6 +10,11 @@ One STEP = one pass of the whole hot path over the Reddit-shaped graph
     a    = edge_softmax(s)     in place    GAT attention        (A6)
     out3 = gspmm_weighted(Z, a, fwd)       GAT aggregate        (A7)
     out4 = gspmm_weighted(dO, a, rev)      GAT backward dZ      (A8)
+With --chain fused (the default) A5-A7 run as ONE kernel (gsp_gat_forward,
+NEXT-2) that leaves the same state behind: a = alpha [E, H] in the same buffer,
+out3 the aggregate -- 4 launches per step; --chain separate runs the six
+calls above.  The separate A5-A7 calls are then timed outside the step
+(per_op, "in_step": false) so every row keeps its own number.
 value = edge visits per second over the step = 6 * E / t_step (GE/s), whole job.
 At N > 1 every rank runs the same step on its destination-row partition and
 all-gathers each vertex-level output over NCCL (A9); scaling is "strong"
@@ -50,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e / cpu baseline / clocks)")
     ap.add_argument("--check", action="store_true", help="N > 1: compare the exchanged outputs with the full graph")
+    ap.add_argument("--chain", choices=["fused", "separate"], default="fused",
+                    help="GAT forward A5-A7 as one fused kernel (default) or three calls")
     return ap.parse_args()
 
 
@@ -68,6 +75,8 @@ def alg_bytes(op, V, E, F, H):
         return base + 4 * V * F + 4 * E * F + 4 * E * H
     if op == "edge_softmax":
         return 8 * (V + 1) + 4 * E * H + 4 * E * H
+    if op == "gat_forward":      # fused A5-A7 (Y == Vt gathered once): alpha written once
+        return base + 4 * V * F + 4 * E * F + 4 * E * H + 4 * V * F
     raise KeyError(op)
 
 
@@ -81,14 +90,14 @@ def load_peaks():
 
 
 def load_traffic(config):
-    """ncu dram bytes per launch of the dominant kernel, from a committed profile summary."""
+    """ncu DRAM bytes (read + write) per launch of each op's kernel, from the committed
+    full-capture summaries (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
+        return {}
     with open(p) as f:
         d = json.load(f)
-    v = d.get(config, {}).get("gspmm_fwd_dram_bytes")
-    return float(v) if v is not None else None
+    return {k: float(v["dram_bytes"]) for k, v in d.get(config, {}).items()}
 
 
 # ------------------------------------------------------------------ clocks
@@ -316,16 +325,21 @@ def main_gsp(args):
     partial = torch.empty((ncols, F), device="cuda") if P > 1 else None
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
-    op_names = ["gspmm_fwd", "gspmm_rev", "gsddmm", "edge_softmax", "gspmm_weighted_fwd", "gspmm_weighted_rev"]
+    fused = args.chain == "fused"
+    op_names = (["gspmm_fwd", "gspmm_rev", "gat_forward", "gspmm_weighted_rev"] if fused else
+                ["gspmm_fwd", "gspmm_rev", "gsddmm", "edge_softmax", "gspmm_weighted_fwd", "gspmm_weighted_rev"])
     ev = {k: [] for k in op_names + ["exchange"]}
 
     # the step as a list of (name, launch, input index into (X, dY, Z, dO) or None, output index or None)
     def op_list():
         L = [("gspmm_fwd", lambda: part.gspmm(X, gsp.NORM_BOTH, out=outs[0], stream=stream), 0, 0),
-             ("gspmm_rev", lambda: part.gspmm(dY, gsp.NORM_BOTH, out=outs[1], reverse=True, stream=stream), 1, 1),
-             ("gsddmm", lambda: part.gsddmm(Z, Z, out=s, stream=stream), 2, None),
-             ("edge_softmax", lambda: part.edge_softmax(s, out=s, stream=stream), None, None),
-             ("gspmm_weighted_fwd", lambda: part.gspmm_weighted(Z, s, out=outs[2], stream=stream), None, 2)]
+             ("gspmm_rev", lambda: part.gspmm(dY, gsp.NORM_BOTH, out=outs[1], reverse=True, stream=stream), 1, 1)]
+        if fused:   # A5-A7 in one pass per destination row; s ends up holding alpha, as below
+            L.append(("gat_forward", lambda: part.gat_forward(Z, Z, Z, H, alpha=s, out=outs[2], stream=stream), 2, 2))
+        else:
+            L += [("gsddmm", lambda: part.gsddmm(Z, Z, out=s, stream=stream), 2, None),
+                  ("edge_softmax", lambda: part.edge_softmax(s, out=s, stream=stream), None, None),
+                  ("gspmm_weighted_fwd", lambda: part.gspmm_weighted(Z, s, out=outs[2], stream=stream), None, 2)]
         if P == 1:
             L.append(("gspmm_weighted_rev",
                       lambda: part.gspmm_weighted(dO, s, out=outs[3], reverse=True, stream=stream), 3, 3))
@@ -509,36 +523,56 @@ def main_gsp(args):
     peak, peak_kind = load_peaks()
     avg = {k: (sum(v) / len(v) if v else None) for k, v in ev.items()}
     Vloc, Eloc = (R, Ep) if P > 1 else (V, E)
+    def time_op(fn, reps=5, flush_l2=True):
+        """median event time of one call (L2 flushed before each), outside the step"""
+        for _ in range(2):
+            fn()
+        ts = []
+        for _ in range(reps):
+            if flush_l2:
+                flush.fill_(1.0)
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            fn()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a0.elapsed_time(a1))
+        return sorted(ts)[len(ts) // 2]
+
+    # rows the step does not launch on their own: timed one by one outside it
+    outside = {}
+    if not args.profile:
+        if fused:   # the unfused A5-A7 calls, each on its own (same graph, same inputs)
+            s2 = torch.empty((Ep, H), device="cuda")
+            g2 = torch.empty((R, F), device="cuda")
+            part.gsddmm(Z, Z, out=s2, stream=stream)
+            outside["gsddmm"] = time_op(lambda: part.gsddmm(Z, Z, out=s2, stream=stream))
+            raw = s2.clone()              # out of place: the same logits every call
+            outside["edge_softmax"] = time_op(lambda: part.edge_softmax(raw, out=s2, stream=stream))
+            outside["gspmm_weighted_fwd"] = time_op(lambda: part.gspmm_weighted(Z, s2, out=g2, stream=stream))
+            del s2, g2, raw
+        else:
+            g2 = torch.empty((R, F), device="cuda")
+            outside["gat_forward"] = time_op(lambda: part.gat_forward(Z, Z, Z, H, alpha=torch.empty_like(s),
+                                                                      out=g2, stream=stream))
+            del g2
+
     # ------------------------------------------- NEXT rows (outside the step)
     next_rows = None
     if not args.profile:
-        def time_op(fn, reps=5, flush_l2=True):
-            for _ in range(2):
-                fn()
-            ts = []
-            for _ in range(reps):
-                if flush_l2:
-                    flush.fill_(1.0)
-                a0 = torch.cuda.Event(enable_timing=True)
-                a1 = torch.cuda.Event(enable_timing=True)
-                a0.record(stream)
-                fn()
-                a1.record(stream)
-                torch.cuda.synchronize()
-                ts.append(a0.elapsed_time(a1))
-            return sorted(ts)[len(ts) // 2]
         alpha2 = torch.empty((Ep, H), device="cuda")
         gout = torch.empty((R, F), device="cuda")
         dal = torch.rand((Ep, H), device="cuda")
-        ms_gat = time_op(lambda: part.gat_forward(Z, Z, Z, H, alpha=alpha2, out=gout, stream=stream))
+        ms_gat = avg["gat_forward"] if fused else outside["gat_forward"]
         ms_max = time_op(lambda: part.gspmm_reduce(X, gsp.REDUCE_MAX, out=gout, stream=stream))
         hout = torch.empty((R, H), device="cuda")
         ms_e = time_op(lambda: part.gspmm_e(s, gsp.REDUCE_SUM, out=hout, stream=stream))
         ms_ve = time_op(lambda: part.gsddmm_ve(Z[:, :H], dal, gsp.OP_ADD, gsp.SIDE_SRC, out=alpha2, stream=stream))
         ms_sbw = time_op(lambda: part.edge_softmax_backward(s, dal, out=dal, stream=stream))
-        sep = avg["gsddmm"] + avg["edge_softmax"] + avg["gspmm_weighted_fwd"]
+        sep = sum((outside if fused else avg)[k] for k in ("gsddmm", "edge_softmax", "gspmm_weighted_fwd"))
         next_rows = {
-            "gat_forward_fused": {"row": "NEXT-2", "ms": round(ms_gat, 4),
+            "gat_forward_fused": {"row": "NEXT-2", "ms": round(ms_gat, 4), "in_step": fused,
                                   "vs_separate_chain_ms": round(sep, 4),
                                   "GE_s": round(Eloc / (ms_gat * 1e-3) / 1e9, 3)},
             "gspmm_reduce_max": {"row": "NEXT-3", "ms": round(ms_max, 4),
@@ -573,17 +607,19 @@ def main_gsp(args):
         del X32, w1, o32
 
     per_op = {}
+    traffic = load_traffic(args.config) if P == 1 else {}
     bytes_of = {"gspmm_fwd": alg_bytes("gspmm", Vloc, Eloc, F, H), "gspmm_rev": alg_bytes("gspmm", Vloc, Eloc, F, H),
                 "gsddmm": alg_bytes("gsddmm", Vloc, Eloc, F, H),
                 "edge_softmax": alg_bytes("edge_softmax", Vloc, Eloc, F, H),
                 "gspmm_weighted_fwd": alg_bytes("gspmm_weighted_fwd", Vloc, Eloc, F, H),
-                "gspmm_weighted_rev": alg_bytes("gspmm_weighted_rev", Vloc, Eloc, F, H)}
-    for k in op_names:
-        ms = avg[k]
+                "gspmm_weighted_rev": alg_bytes("gspmm_weighted_rev", Vloc, Eloc, F, H),
+                "gat_forward": alg_bytes("gat_forward", Vloc, Eloc, F, H)}
+    for k, ms in [(k, avg[k]) for k in op_names] + list(outside.items()):
         gbs = bytes_of[k] / (ms * 1e-3) / 1e9
         per_op[k] = {"ms": round(ms, 4), "GE_s": round(Eloc / (ms * 1e-3) / 1e9, 3), "alg_GB": round(bytes_of[k] / 1e9, 3),
                      "GB_s": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
-                     "frac_of_8TBs": round(gbs / 8000.0, 4)}
+                     "frac_of_8TBs": round(gbs / 8000.0, 4), "in_step": k in op_names,
+                     "traffic_GB": round(traffic[k] / 1e9, 3) if k in traffic else None}
     if P > 1:
         per_op["exchange"] = {"ms": round(avg["exchange"], 4),
                               "what": "3 x all_gather_into_tensor [R,F] + reduce_scatter_tensor [P*R,F] "
@@ -594,7 +630,7 @@ def main_gsp(args):
                 "achieved": achieved, "peak": peak, "peak_kind": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                 "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "alg_bytes_per_launch": bytes_of[dom],
-                "traffic": load_traffic(args.config)}
+                "traffic": traffic.get(dom)}
 
     cpu = None
     if rank == 0 and P == 1 and not args.no_cpu_baseline and not args.profile:
@@ -613,6 +649,8 @@ def main_gsp(args):
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{cfg.name}-shaped GCN gSpMM fwd+bwd (BOTH norm) + GAT chain "
                                    f"(gSDDMM u.v, edge softmax, weighted gSpMM fwd+rev), F={F}, H={H}x{cfg.Fh}",
+                       "gat_chain": ("fused: gSDDMM + edge softmax + weighted gSpMM fwd in one kernel "
+                                     "(gsp_gat_forward; alpha still written)") if fused else "separate: 3 kernels",
                        "V": V, "E": E, "F": F, "H": H, "Fh": cfg.Fh,
                        "graph": f"Chung-Lu beta={cfg.beta}, seed={cfg.seed:#x}" if cfg.kind == "chung_lu"
                        else f"R-MAT scale {cfg.scale}, seed={cfg.seed:#x}",
@@ -627,7 +665,7 @@ def main_gsp(args):
             "multi_gpu_check": check,
             "small_config_latency": latency,
             "e2e": e2e,
-            "gpu_launches": (6 * args.steps),
+            "gpu_launches": (len(OPS) * args.steps),
             "clocks": clk,
             "timing": {"wall_s_timed_region": round(wall, 3),
                        "host_launch_ms_per_step": round(sum(host_launch_ms) / len(host_launch_ms), 3), "graph_gen_s": round(t_gen, 2),

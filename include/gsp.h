@@ -75,9 +75,18 @@ enum {
     GSP_BUILD_SHARE_SYMMETRIC = 1u << 1,  /* if the edge multiset is symmetric, keep ONE topology for
                                              fwd and rev ("one copy of the topology"); rev_eid
                                              is still stored */
-    GSP_BUILD_EDGE_SCALES = 1u << 2       /* precompute the per-edge column-side degree scale of the BOTH
+    GSP_BUILD_EDGE_SCALES = 1u << 2,      /* precompute the per-edge column-side degree scale of the BOTH
                                              norm (4 B per edge per structure; one array when symmetric)
                                              so gsp_gspmm streams it instead of gathering d^-1/2 per edge */
+    GSP_BUILD_L2_PERSIST = 1u << 3        /* opt-in: raise the device's persisting-L2 set-aside
+                                             (cudaLimitPersistingL2CacheSize, device-wide, never lowered)
+                                             to min(device maximum, 48 MiB; env GSP_L2_SETASIDE_MB
+                                             overrides).  The gathered feature tables are loaded with an
+                                             L2 evict_last policy, which only protects lines inside the
+                                             set-aside from the edge-tensor streams: gSDDMM and the fused
+                                             GAT forward gain ~5 %, but edge softmax (+10-15 %), its
+                                             backward and gSDDMMve lose the L2 capacity they reuse
+                                             (DESIGN.md §6).  A failure to set it is ignored (cache hint) */
 };
 
 /* gsp_graph_partition flags */

@@ -116,14 +116,7 @@ gsp_status upload_structure(gsp_graph *g, gsp::DevStructure &S, int64_t nrows, i
         if ((st = dev_upload(g, col.data(), col.size(), &S.col)) != GSP_OK) return st;
     }
     if (eid && (st = dev_upload(g, eid->data(), eid->size(), &S.eid)) != GSP_OK) return st;
-    if (shared_order) {   // same offsets (symmetric topology): same schedule
-        S.order = shared_order;
-        S.task = share_topology->task;
-        S.n_heavy = shared_n_heavy;
-    } else {
-        std::vector<int32_t> order;
-        gsp::degree_order(off.data(), nrows, gsp::kHeavyThreshold, order, S.n_heavy);
-        if ((st = dev_upload(g, order.data(), order.size(), &S.order)) != GSP_OK) return st;
+    auto make_task = [&](const std::vector<int32_t> &order, const int32_t **dst) {
         std::vector<int32_t> task((size_t)nrows * 4);
         for (int64_t i = 0; i < nrows; i++) {
             const int64_t r = order[i], b = off[r];
@@ -132,10 +125,37 @@ gsp_status upload_structure(gsp_graph *g, gsp::DevStructure &S, int64_t nrows, i
             task[4 * i + 2] = (int32_t)(uint32_t)((uint64_t)b & 0xffffffffu);
             task[4 * i + 3] = (int32_t)(uint32_t)((uint64_t)b >> 32);
         }
-        if ((st = dev_upload(g, task.data(), task.size(), &S.task)) != GSP_OK) return st;
+        return dev_upload(g, task.data(), task.size(), dst);
+    };
+    std::vector<int32_t> order;
+    if (shared_order) {   // same offsets (symmetric topology): same schedule
+        S.order = shared_order;
+        S.task = share_topology->task;
+        S.n_heavy = shared_n_heavy;
+        if (eid) gsp::degree_order(off.data(), nrows, gsp::kHeavyThreshold, order, S.n_heavy);
+    } else {
+        gsp::degree_order(off.data(), nrows, gsp::kHeavyThreshold, order, S.n_heavy);
+        if ((st = dev_upload(g, order.data(), order.size(), &S.order)) != GSP_OK) return st;
+        if ((st = make_task(order, &S.task)) != GSP_OK) return st;
+    }
+    static const int64_t win = [] {   // GSP_EID_WIN: id window of the locality schedule (0: off)
+        const char *e = getenv("GSP_EID_WIN");
+        return e ? atoll(e) : int64_t(2048);
+    }();
+    if (eid && win > 0) {   // locality schedule for the edge-ID indirected reverse (graph.h)
+        std::sort(order.begin() + S.n_heavy, order.end(), [&](int32_t a, int32_t b) {
+            const int64_t wa = a / win, wb = b / win;
+            if (wa != wb) return wa < wb;
+            const int64_t da = off[a + 1] - off[a], db = off[b + 1] - off[b];
+            return da != db ? da > db : a < b;
+        });
+        if ((st = make_task(order, &S.task_id)) != GSP_OK) return st;
     }
     return GSP_OK;
 }
+
+// schedule of the edge-ID indirected reverse ops (graph.h task_id)
+const int32_t *eid_task(const gsp::DevStructure &S) { return S.task_id ? S.task_id : S.task; }
 
 std::vector<int64_t> degrees_of(const std::vector<int64_t> &off) {
     std::vector<int64_t> d(off.empty() ? 0 : off.size() - 1);
@@ -283,13 +303,31 @@ static gsp_status upload_full(gsp_graph *g) {
     return GSP_OK;
 }
 
+// GSP_BUILD_L2_PERSIST (include/gsp.h): a cache hint, so failures are ignored
+void raise_l2_setaside(int device) {
+    DeviceGuard dg(device);
+    int maxp = 0;
+    if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) != cudaSuccess || maxp <= 0) {
+        cudaGetLastError();
+        return;
+    }
+    const char *env = getenv("GSP_L2_SETASIDE_MB");
+    size_t want = (size_t)(env ? atoll(env) : 48) << 20;
+    if (want > (size_t)maxp) want = (size_t)maxp;
+    size_t cur = 0;
+    if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess && cur < want)
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    cudaGetLastError();
+}
+
 gsp_status gsp_graph_create(int64_t V, int64_t E, const int64_t *src, const int64_t *dst, uint32_t flags,
                             int device, gsp_graph **g_out) {
     if (!g_out) return fail(GSP_ERR_NULL, "g_out is NULL");
     *g_out = nullptr;
     if (E > 0 && (!src || !dst)) return fail(GSP_ERR_NULL, "src/dst is NULL");
     if (V < 0 || E < 0) return fail(GSP_ERR_ARG, "V and E must be >= 0");
-    if (flags & ~(uint32_t)(GSP_BUILD_REVERSE | GSP_BUILD_SHARE_SYMMETRIC | GSP_BUILD_EDGE_SCALES))
+    if (flags & ~(uint32_t)(GSP_BUILD_REVERSE | GSP_BUILD_SHARE_SYMMETRIC | GSP_BUILD_EDGE_SCALES |
+                            GSP_BUILD_L2_PERSIST))
         return fail(GSP_ERR_ARG, "unknown flags");
     if (V >= (int64_t(1) << 31) || E >= (int64_t(1) << 31))
         return fail(GSP_ERR_OVERFLOW, "V and E must be < 2^31 (int32 column and edge ids)");
@@ -319,6 +357,7 @@ gsp_status gsp_graph_create(int64_t V, int64_t E, const int64_t *src, const int6
     g->symmetric = g->host.symmetric;
     g->device = device;
     g->edge_scales = (flags & GSP_BUILD_EDGE_SCALES) != 0;
+    if (device >= 0 && (flags & GSP_BUILD_L2_PERSIST)) raise_l2_setaside(device);
     if (device >= 0) {
         st = upload_full(g);
         if (st != GSP_OK) {
@@ -416,7 +455,7 @@ gsp_status gsp_gspmm_weighted(const gsp_graph *g, const gsp_tensor *X, const gsp
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SpmmArgs a{};
-    a.off = S.off; a.col = S.col; a.eid = S.eid; a.order = S.order; a.task = S.task;
+    a.off = S.off; a.col = S.col; a.eid = S.eid; a.order = S.order; a.task = reverse ? eid_task(S) : S.task;
     a.nrows = S.nrows; a.n_heavy = S.n_heavy;
     a.X = static_cast<const float *>(X->data); a.ldx = X->ld;
     a.out = static_cast<float *>(out->data); a.ldo = out->ld;
@@ -618,7 +657,8 @@ gsp_status gsp_gspmm_e(const gsp_graph *g, const gsp_tensor *w, int reduce, gsp_
     if ((st = check_stream(g, stream)) != GSP_OK) return st;
     DeviceGuard dg(g->device);
     gsp::SpmmEArgs a{};
-    a.off = S.off; a.eid = reverse ? S.eid : nullptr; a.order = S.order; a.task = S.task; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.off = S.off; a.eid = reverse ? S.eid : nullptr; a.order = S.order; a.task = reverse ? eid_task(S) : S.task;
+    a.nrows = S.nrows; a.n_heavy = S.n_heavy;
     a.w = static_cast<const float *>(w->data); a.ldw = w->ld;
     a.out = static_cast<float *>(out->data); a.ldo = out->ld;
     a.H = w->cols; a.red = reduce;

@@ -51,6 +51,13 @@ struct DevStructure {
     // the same schedule as 16-B records {row, degree, off[row] lo, hi}: one
     // vector load gives a warp its whole task (no order -> off round trip)
     const int32_t *task = nullptr;
+    // structures with explicit edge ids (rev, lrev): the same heavy rows first,
+    // then the light rows in windows of consecutive row ids (by descending degree
+    // inside a window, so a CTA's 8 warps get rows of similar length).  Rows in
+    // flight together then cover a narrow range of ids, so the edge-ID indirected
+    // reads of a destination's edge block (w[eid]: contiguous per destination,
+    // ordered by source id) hit the same lines close in time.
+    const int32_t *task_id = nullptr;
     int64_t n_heavy = 0;
     int64_t max_deg = 0;
     bool present = false;

@@ -21,7 +21,7 @@ NORM_NONE, NORM_RIGHT, NORM_BOTH = 0, 1, 2
 REDUCE_SUM, REDUCE_MIN, REDUCE_MAX = 0, 1, 2
 OP_ADD, OP_SUB, OP_MUL, OP_DIV = 0, 1, 2, 3
 SIDE_DST, SIDE_SRC = 0, 1
-BUILD_REVERSE, BUILD_SHARE_SYMMETRIC, BUILD_EDGE_SCALES = 1, 2, 4
+BUILD_REVERSE, BUILD_SHARE_SYMMETRIC, BUILD_EDGE_SCALES, BUILD_L2_PERSIST = 1, 2, 4, 8
 PART_REVERSE = 1
 
 STATUS = {0: "GSP_OK", 1: "GSP_ERR_NULL", 2: "GSP_ERR_ARG", 3: "GSP_ERR_VERTEX_RANGE", 4: "GSP_ERR_SHAPE",
@@ -114,8 +114,8 @@ def _stream(stream, device):
 class Graph:
     """Kernel-graph handle (GraphPy's `g`) owning a libgsp graph."""
 
-    def __init__(self, V=None, src=None, dst=None, *, reverse=True, share_symmetric=True, edge_scales=True, device=0,
-                 _handle=None):
+    def __init__(self, V=None, src=None, dst=None, *, reverse=True, share_symmetric=True, edge_scales=True,
+                 l2_persist=False, device=0, _handle=None):
         self._h = ctypes.c_void_p()
         if _handle is not None:
             self._h = _handle
@@ -125,7 +125,7 @@ class Graph:
             if src.shape != dst.shape or src.ndim != 1:
                 raise ValueError("src and dst must be 1-D arrays of equal length")
             flags = (BUILD_REVERSE if reverse else 0) | (BUILD_SHARE_SYMMETRIC if share_symmetric else 0) | \
-                (BUILD_EDGE_SCALES if edge_scales else 0)
+                (BUILD_EDGE_SCALES if edge_scales else 0) | (BUILD_L2_PERSIST if l2_persist else 0)
             _check(lib.gsp_graph_create(int(V), src.shape[0], src.ctypes.data, dst.ctypes.data, flags,
                                         int(device), ctypes.byref(self._h)))
         V_, E_, b_, s_ = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()

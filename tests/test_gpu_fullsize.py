@@ -98,6 +98,30 @@ def test_reddit_gat_chain_sampled(reddit):
         within(out[rows], ref, T)
 
 
+def test_reddit_gat_forward_fused_sampled(reddit):
+    """The fused GAT forward in bench.py's step configuration (gat_forward(Z, Z, Z),
+    H = 8 x 8, alpha into a preallocated [E, H] buffer): alpha and the aggregate of
+    sampled rows against oracle C10.  A row's results depend only on its own
+    in-edges, so the oracle runs on the sub-graph of the sampled rows' in-edges
+    (same vertex ids; its fwd slots are the rows' slots in order)."""
+    cfg, G, og = reddit
+    H, F = cfg.H, cfg.H * cfg.Fh
+    rows = sample_rows(og.fwd_off, 91)
+    eids = og.row_edges(rows)
+    sub_dst = np.repeat(rows, og.fwd_off[rows + 1] - og.fwd_off[rows])
+    sub = oracle.Graph(og.V, og.fwd_col[eids].astype(np.int64), sub_dst)
+    assert np.array_equal(sub.fwd_col, og.fwd_col[eids])
+    Zh = datagen.uniform(17, og.V, F)
+    Z = dev(Zh)
+    alpha = torch.empty((og.E, H), device="cuda")
+    out = torch.empty((og.V, F), device="cuda")
+    G.gat_forward(Z, Z, Z, H, alpha=alpha, out=out)
+    a_ref, o_ref, T = sub.gat_forward(Zh, Zh, Zh, H)
+    # tolerances as the small-size fused tests (DESIGN.md "Tolerances")
+    within(alpha[torch.from_numpy(eids).cuda()].cpu().numpy(), a_ref, 1.0)   # 2e-5 absolute
+    within(out[torch.from_numpy(rows).cuda()].cpu().numpy(), o_ref[rows], T[rows], scale=2e-5)
+
+
 def test_products_gspmm_sampled():
     import paper_2402_03548_b200 as gsp
     cfg = datagen.CONFIGS["products"]
