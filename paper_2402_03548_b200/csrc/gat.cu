@@ -11,9 +11,13 @@ namespace {
 // head, Fh = 8 features per lane):
 //   s = <X[v,h], Y[u,h]>          -> written to alpha (raw) ;
 //   online softmax (m, S) and acc = sum exp(s - m) Vt[u,h]   (flash-style);
-// then out[v,h] = acc / S and the row's raw scores are re-read (L2-hot) and
-// overwritten with alpha = exp(s - m) / S.  Y and Vt may be the same table
-// (one gather serves both).  Heavy rows: CTA split + deterministic merge.
+// then out[v,h] = acc / S and the row's raw scores are re-read and
+// overwritten with alpha = exp(s - m) / S.  The first `cap` edges of each
+// warp's slice keep their raw scores in shared memory (dynamic, cap * H floats
+// per warp): only the excess of long rows makes the global round trip, so the
+// in-flight score blocks no longer crowd the gathered table out of L2.  Y and
+// Vt may be the same table (one gather serves both).  Heavy rows: CTA split +
+// deterministic merge.
 template <int LPE, bool SAME>
 __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a) {
     constexpr int VEC = 8;
@@ -27,6 +31,7 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
     // [t][lane]: lane-minor, so the per-lane accesses are bank-conflict free
     __shared__ __align__(16) float s_run[kWarps][2 * VEC][32];
     __shared__ float sm_ms[kWarps][LPE][2];
+    extern __shared__ __align__(16) float s_sc[];   // [kWarps][cap][H] raw scores
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / LPE, h = lane % LPE;   // head of this lane
     const int H = LPE;
@@ -35,6 +40,8 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
     bool heavy;
     if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
     const Pol pol = make_pol();
+    const int64_t cap = a.sc_cap;
+    float *wsc = s_sc + (int64_t)warp * cap * LPE;
 
     Vec<VEC> xv;
     ld_keep(xv, a.X + (a.row_base + row) * a.ldx + h * VEC, pol.stream);
@@ -60,7 +67,11 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
         c2 = load_col(base + 64);
         __syncwarp();
         const int *gp = &s_col[warp][g * PER];
-        float *ab = a.alpha + (base + g) * H + h;   // group g's i-th edge is tile edge g + G*i
+        // raw scores of this tile: shared memory while the slice is within cap (whole
+        // tiles: cap is a multiple of 32), else the alpha buffer itself
+        const bool in_smem = base - b < cap;
+        float *ab = in_smem ? wsc + (base - b + g) * H + h
+                            : a.alpha + (base + g) * H + h;   // group g's i-th edge is tile edge g + G*i
         const int mcount = n == 32 ? PER : (n > g ? (n - g + G - 1) / G : 0);
         auto body = [&](int i, auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
@@ -100,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
                 }
                 sc[u] = s0 + s1;
                 if (FULL || i + u < mcount) {
-                    ab[(int64_t)(G * (i + u)) * H] = sc[u];   // raw score (default L2 policy), re-read below
+                    ab[(int64_t)(G * (i + u)) * H] = sc[u];   // raw score (smem, or global with the default L2 policy)
                     mb = fmaxf(mb, sc[u]);
                 } else {
                     sc[u] = -INFINITY;
@@ -203,9 +214,10 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
         for (int t = 0; t < VEC; t++) r.v[t] = acc.v[t] * rS;
         vstore(a.out + row * a.ldo + h * VEC, r, VEC);
     }
-    // normalise this warp's slice of raw scores in place: element i has head i % H
+    // normalise this warp's slice of raw scores into alpha: element i has head i % H;
+    // [lo, mid) from shared memory, [mid, hi) in place in global memory
     __syncwarp();
-    const int64_t lo = b * H, hi = e * H;
+    const int64_t lo = b * H, hi = e * H, mid = min(hi, lo + cap * H);
     if (H % 4 == 0) {
         float mh[4], rh[4];
 #pragma unroll
@@ -214,8 +226,15 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
             mh[t] = __shfl_sync(kFull, m, hh);
             rh[t] = __shfl_sync(kFull, rS, hh);
         }
+        for (int64_t i0 = lo + (int64_t)lane * 4; i0 < mid; i0 += 128) {
+            const float4 v = *reinterpret_cast<const float4 *>(wsc + (i0 - lo));
+            st_stream_f4(a.alpha + i0,
+                         make_float4(fast_exp(v.x - mh[0]) * rh[0], fast_exp(v.y - mh[1]) * rh[1],
+                                     fast_exp(v.z - mh[2]) * rh[2], fast_exp(v.w - mh[3]) * rh[3]),
+                         pol.stream);
+        }
         constexpr int NU = 8;   // loads in flight per lane (the row block is L2-hot)
-        for (int64_t i0 = lo + (int64_t)lane * 4; i0 < hi; i0 += 128 * NU) {
+        for (int64_t i0 = mid + (int64_t)lane * 4; i0 < hi; i0 += 128 * NU) {
             float4 v[NU];
 #pragma unroll
             for (int k = 0; k < NU; k++)
@@ -232,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
         const int hh = lane % H;
         const float mh = __shfl_sync(kFull, m, hh), rh = __shfl_sync(kFull, rS, hh);
         for (int64_t i = lo + lane; i < hi; i += 32) {
-            const float v = ld_f32(a.alpha + i, pol.stream);
+            const float v = i < mid ? wsc[i - lo] : ld_f32(a.alpha + i, pol.stream);
             st_stream_f32(a.alpha + i, fast_exp(v - mh) * rh, pol.stream);
         }
     }
@@ -247,26 +266,46 @@ bool gat_fused_supported(const GatArgs &a) {
            aligned(a.Y, 32) && aligned(a.Vt, 32) && aligned(a.out, 16) && aligned(a.alpha, 16);
 }
 
+// shared-memory score block per warp (bytes); GSP_GAT_SMEM_KB overrides (0: off, A/B)
+static int64_t gat_score_bytes() {
+    static const int64_t v = [] {
+        const char *e = getenv("GSP_GAT_SMEM_KB");
+        return (e ? atoll(e) : int64_t(6)) << 10;   // 6 KB: 3.26 -> 3.02 ms on Reddit 8x8; 11 KB: 4.2 ms (L1 squeezed)
+    }();
+    return v;
+}
+
+template <int HH, bool SAME>
+cudaError_t launch_gat_h(GatArgs a, dim3 grid, cudaStream_t s) {
+    a.sc_cap = (gat_score_bytes() / (4 * HH)) & ~int64_t(31);   // whole 32-edge tiles
+    const size_t dyn = (size_t)(kWarps * a.sc_cap * HH * 4);
+    static bool attr[64] = {};   // opt in to > 48 KB of dynamic shared memory once per device
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 64 || !attr[dev]) {
+        e = cudaFuncSetAttribute(gat_fused_kernel<HH, SAME>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (e != cudaSuccess) return e;
+        if (dev < 64) attr[dev] = true;
+    }
+    gat_fused_kernel<HH, SAME><<<grid, kThreads, dyn, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gat_fused(const GatArgs &a, cudaStream_t s) {
     if (a.nrows == 0) return cudaSuccess;
     const dim3 grid = row_grid(a.nrows, a.n_heavy, 1);
     const bool same = a.Vt == a.Y && a.ldv == a.ldy;
-#define GSP_GAT_CASE(HH)                                                         \
-    case HH:                                                                     \
-        if (same) gat_fused_kernel<HH, true><<<grid, kThreads, 0, s>>>(a);       \
-        else gat_fused_kernel<HH, false><<<grid, kThreads, 0, s>>>(a);           \
-        break;
+#define GSP_GAT_CASE(HH) \
+    case HH: return same ? launch_gat_h<HH, true>(a, grid, s) : launch_gat_h<HH, false>(a, grid, s);
     switch (a.H) {
         GSP_GAT_CASE(2)
         GSP_GAT_CASE(4)
         GSP_GAT_CASE(8)
         GSP_GAT_CASE(16)
-        default:
-            if (same) gat_fused_kernel<32, true><<<grid, kThreads, 0, s>>>(a);
-            else gat_fused_kernel<32, false><<<grid, kThreads, 0, s>>>(a);
+        default: return same ? launch_gat_h<32, true>(a, grid, s) : launch_gat_h<32, false>(a, grid, s);
     }
 #undef GSP_GAT_CASE
-    return cudaGetLastError();
 }
 
 }  // namespace gsp

@@ -97,6 +97,7 @@ struct GatArgs {
     float *out;
     int64_t ldo;
     int64_t H;
+    int64_t sc_cap;    // edges per warp slice whose raw scores stay in shared memory (set by the launcher)
 };
 bool gat_fused_supported(const GatArgs &a);
 cudaError_t launch_gat_fused(const GatArgs &a, cudaStream_t s);
