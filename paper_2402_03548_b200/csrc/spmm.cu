@@ -494,8 +494,13 @@ template <int VEC, int LPE, int CPL>
 cudaError_t spmm_go(const SpmmArgs &a, int mode, int64_t slabs, cudaStream_t s) {
     if constexpr (VEC == 8 && LPE == 8 && CPL == 1) {
         switch (tune_spmm()) {
-            case 0:   // measured best on B200 (Reddit-shaped F = 64, tools/opbench.py)
+            case 0:   // measured best on B200 (Reddit-shaped F = 64, tools/opbench.py): the scaled
+                      // gSpMM 4 gathers in flight per lane at 3 CTAs/SM (1.63 ms; 4 CTAs/SM 1.63-1.66,
+                      // 8 at 2 CTAs/SM 1.69); the weighted modes 8 at 2 CTAs/SM (wfwd 2.01 vs 2.39,
+                      // wrev 2.84 vs 3.72 ms at 4 / 4)
+                if (mode == kSpmmScaled) return spmm_go_v<VEC, LPE, CPL, 4, 3>(a, mode, slabs, s);
                 return spmm_go_v<VEC, LPE, CPL, 8, 2>(a, mode, slabs, s);
+            case 7: return spmm_go_v<VEC, LPE, CPL, 4, 3>(a, mode, slabs, s);
             case 5: return spmm_go_v<VEC, LPE, CPL>(a, mode, slabs, s);
             case 6: return spmm_go_v<VEC, LPE, CPL, 4, 2>(a, mode, slabs, s);
             case 1: return spmm_go_v<VEC, LPE, CPL, 8, 2>(a, mode, slabs, s);
