@@ -642,7 +642,7 @@ def main_gsp(args):
                                       + ("(NCCL)" if backend == "nccl" else "(host-staged gloo: validation only)")}
     dom = "gspmm_fwd"
     achieved = per_op[dom]["GB_s"]
-    roofline = {"bound": "hbm", "kernel": "spmm_kernel<VEC=8,LPE=8,CPL=1,scaled> (gspmm fwd, BOTH norm)",
+    roofline = {"bound": "hbm", "kernel": "spmm_kernel<VEC=8,LPE=8,CPL=1,scaled,U=4,3 CTAs/SM> (gspmm fwd, BOTH norm)",
                 "achieved": achieved, "peak": peak, "peak_kind": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                 "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "alg_bytes_per_launch": bytes_of[dom],
