@@ -61,6 +61,22 @@ def parse():
 
 
 # ------------------------------------------------------------- byte models
+def step_config(cfg, V, E, P, fused):
+    """The workload description both arms print (the reference arm runs the same step)."""
+    F, H = cfg.H * cfg.Fh, cfg.H
+    return {"workload": f"{cfg.name}-shaped GCN gSpMM fwd+bwd (BOTH norm) + GAT chain "
+                        f"(gSDDMM u.v, edge softmax, weighted gSpMM fwd+rev), F={F}, H={H}x{cfg.Fh}",
+            "gat_chain": ("fused: gSDDMM + edge softmax + weighted gSpMM fwd in one kernel "
+                          "(gsp_gat_forward; alpha still written)") if fused else "separate: 3 kernels",
+            "V": V, "E": E, "F": F, "H": H, "Fh": cfg.Fh,
+            "graph": f"Chung-Lu beta={cfg.beta}, seed={cfg.seed:#x}" if cfg.kind == "chung_lu"
+            else f"R-MAT scale {cfg.scale}, seed={cfg.seed:#x}",
+            "parallelism": f"row-partition x{P}" if P > 1 else "single GPU",
+            "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write); "
+                  f"per-step inputs (col ids {4 * E / 1e9:.2f} GB, alpha {4 * E * H / 1e9:.2f} GB) exceed L2",
+            "edge_visits_per_step": N_OPS * E}
+
+
 def alg_bytes(op, V, E, F, H):
     """Algorithmic (compulsory) bytes per launch: every
     gathered feature row counted once per edge, indices/values/outputs once."""
@@ -670,17 +686,7 @@ def main_gsp(args):
             "n_gpus": P, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}-shaped GCN gSpMM fwd+bwd (BOTH norm) + GAT chain "
-                                   f"(gSDDMM u.v, edge softmax, weighted gSpMM fwd+rev), F={F}, H={H}x{cfg.Fh}",
-                       "gat_chain": ("fused: gSDDMM + edge softmax + weighted gSpMM fwd in one kernel "
-                                     "(gsp_gat_forward; alpha still written)") if fused else "separate: 3 kernels",
-                       "V": V, "E": E, "F": F, "H": H, "Fh": cfg.Fh,
-                       "graph": f"Chung-Lu beta={cfg.beta}, seed={cfg.seed:#x}" if cfg.kind == "chung_lu"
-                       else f"R-MAT scale {cfg.scale}, seed={cfg.seed:#x}",
-                       "parallelism": f"row-partition x{P}" if P > 1 else "single GPU",
-                       "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write); "
-                             f"per-step inputs (col ids {4 * E / 1e9:.2f} GB, alpha {4 * E * H / 1e9:.2f} GB) exceed L2",
-                       "edge_visits_per_step": N_OPS * E},
+            "config": step_config(cfg, V, E, P, fused),
             "per_op": per_op,
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -710,16 +716,16 @@ def main_reference(args):
     V, src, dst = datagen.make_graph(cfg)
     target = 1_000_000
     r = cpu_oracle_bench(V, src, dst, cfg, target_edges=target, steps=args.steps, warmup=args.warmup)
-    sample = (f"per step: the 6 ops by the fp64 C oracle (1 thread) on the edges of a random "
-              f"{r['E_sample'] / len(src):.2%} of destination rows ({r['E_sample']} of {len(src)} edges)")
+    sample = (f"per step: the 6 ops by the fp64 C oracle (1 thread; C4 x2, C6, C7, C5 x2: the state the "
+              f"fused chain leaves) on the edges of a random {r['E_sample'] / len(src):.2%} of destination rows "
+              f"({r['E_sample']} of {len(src)} edges); value = 6 x sampled edges / step time")
     line = {
         "impl": "reference",
         "metric": "gSpMM GE/s & HBM GB/s (% of 8 TB/s), Reddit-shape F=64, 1/2/4/8 B200",
         "value": round(r["value"], 6), "unit": "GE/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(r["t_step"] * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}-shaped step (6 sparse ops) on a bounded row sample",
-                   "V": V, "E": int(len(src)), "E_sample": r["E_sample"]},
+        "config": step_config(cfg, V, int(len(src)), args.gpus, args.chain == "fused"),
         "cpu_baseline": {"value": round(r["value"], 6), "unit": "GE/s", "cores": 1, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": round(r["value"], 6), "unit": "GE/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
