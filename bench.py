@@ -676,7 +676,9 @@ def main_gsp(args):
         per_op[k] = {"ms": round(ms, 4), "GE_s": round(Eloc / (ms * 1e-3) / 1e9, 3), "alg_GB": round(bytes_of[k] / 1e9, 3),
                      "GB_s": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
                      "frac_of_8TBs": round(gbs / 8000.0, 4), "in_step": k in op_names,
-                     "traffic_GB": round(traffic[k] / 1e9, 3) if k in traffic else None}
+                     "traffic_GB": round(traffic[k] / 1e9, 3) if k in traffic else None,
+                     # SURVEY §8(d) "reuse = B_alg / DRAM bytes" (> 1: the gathers are L2-served)
+                     "reuse": round(bytes_of[k] / traffic[k], 2) if traffic.get(k) else None}
     if P > 1:
         per_op["exchange"] = {"ms": round(avg["exchange"], 4),
                               "what": "3 x all_gather_into_tensor [R,F] + reduce_scatter_tensor [P*R,F] "
