@@ -97,6 +97,15 @@ gsp_status make_scales(gsp_graph *g, const std::vector<int64_t> &deg, const floa
     return GSP_OK;
 }
 
+// rows above this degree get a whole CTA (graph.h kHeavyThreshold; env GSP_HEAVY for A/B)
+int64_t heavy_threshold() {
+    static const int64_t v = [] {
+        const char *e = getenv("GSP_HEAVY");
+        return e ? atoll(e) : gsp::kHeavyThreshold;
+    }();
+    return v;
+}
+
 gsp_status upload_structure(gsp_graph *g, gsp::DevStructure &S, int64_t nrows, int64_t ncols,
                             const std::vector<int64_t> &off, const std::vector<int32_t> &col,
                             const std::vector<int32_t> *eid, const int32_t *shared_order,
@@ -132,9 +141,9 @@ gsp_status upload_structure(gsp_graph *g, gsp::DevStructure &S, int64_t nrows, i
         S.order = shared_order;
         S.task = share_topology->task;
         S.n_heavy = shared_n_heavy;
-        if (eid) gsp::degree_order(off.data(), nrows, gsp::kHeavyThreshold, order, S.n_heavy);
+        if (eid) gsp::degree_order(off.data(), nrows, heavy_threshold(), order, S.n_heavy);
     } else {
-        gsp::degree_order(off.data(), nrows, gsp::kHeavyThreshold, order, S.n_heavy);
+        gsp::degree_order(off.data(), nrows, heavy_threshold(), order, S.n_heavy);
         if ((st = dev_upload(g, order.data(), order.size(), &S.order)) != GSP_OK) return st;
         if ((st = make_task(order, &S.task)) != GSP_OK) return st;
     }

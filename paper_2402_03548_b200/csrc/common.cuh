@@ -5,7 +5,7 @@
 // run on the LSU / L2 path, not on tensor cores.  Common
 // structure:
 //   * rows come from a degree-ordered schedule built at graph create (rows by
-//     descending degree, LPT order): the first n_heavy rows (degree > 1024)
+//     descending degree, LPT order): the first n_heavy rows (degree > kHeavyThreshold = 2048)
 //     get a whole CTA (8 warps split the row's edge list, deterministic smem
 //     combine), the rest one warp each (8 rows per CTA);
 //   * a warp walks its edge list in 32-edge tiles: one coalesced load of 32

@@ -107,7 +107,7 @@ def test_gspmm_random_graphs(gsp, F, ld):
 
 
 def test_gspmm_heavy_and_mega_rows(gsp):
-    """Rows far above the 1024-edge CTA threshold (CTA-split path), rows in every
+    """Rows far above the 2048-edge CTA threshold (CTA-split path), rows in every
     degree bin, isolated vertices; non-negative inputs (the error-growth case of
     SURVEY Appendix B)."""
     V, E = 4000, 600_000
@@ -518,12 +518,13 @@ def test_gsddmm_ve(gsp, H):
 @pytest.mark.parametrize("H,ld", [(8, 8), (8, 12), (8, 10), (16, 20), (4, 4)])
 def test_next3_heavy_rows_and_strides(gsp, H, ld):
     """gSpMMe / gSDDMMve on a graph with CTA-split hub rows (degree 3000 and
-    1025, just past the 1024-edge heavy threshold), empty rows and ragged
-    light rows; edge-value rows padded to ld (NaN padding: never read)."""
+    2049, just past the 2048-edge heavy threshold; 1025, a long warp row),
+    empty rows and ragged light rows; edge-value rows padded to ld (NaN
+    padding: never read)."""
     rng = np.random.default_rng(H * 100 + ld)
     V = 3100
-    hub_src = rng.integers(0, V, 3000 + 1025)
-    hub_dst = np.concatenate([np.zeros(3000, np.int64), np.full(1025, 7, np.int64)])
+    hub_src = rng.integers(0, V, 3000 + 1025 + 2049)
+    hub_dst = np.concatenate([np.zeros(3000, np.int64), np.full(1025, 7, np.int64), np.full(2049, 11, np.int64)])
     m = 6000
     s2, d2 = rng.integers(0, V, m), rng.integers(20, V - 20, m)
     src = np.concatenate([hub_src, s2]).astype(np.int64)
@@ -557,8 +558,8 @@ def test_next3_heavy_rows_and_strides(gsp, H, ld):
 # ------------------------------------------------ tile / bin boundary degrees
 def _boundary_graph():
     """Destination rows with degrees exactly at the kernels' tile (32), fold
-    (4 x 32) and heavy-bin (1024) boundaries, plus empty rows; sources random."""
-    degs = [0, 1, 2, 31, 32, 33, 63, 64, 65, 127, 128, 129, 1023, 1024, 1025, 2047, 2048, 4097, 0, 7]
+    (4 x 32) and heavy-bin (2048; formerly 1024) boundaries, plus empty rows; sources random."""
+    degs = [0, 1, 2, 31, 32, 33, 63, 64, 65, 127, 128, 129, 1023, 1024, 1025, 2047, 2048, 2049, 4097, 0, 7]
     V = 300
     rng = np.random.default_rng(5)
     dst = np.concatenate([np.full(d, v, np.int64) for v, d in enumerate(degs)])
