@@ -350,6 +350,7 @@ def main_gsp(args):
         return Xp
 
     X, dY, Z, dO = (padded_input(cfg.seed + k) for k in range(4))
+    X_, dY_, Z_, dO_ = X, dY, Z, dO
     Ep = part.E
     s = torch.empty((Ep, H), device="cuda")
     outs = [torch.empty((R, F), device="cuda") for _ in range(4)]
@@ -363,7 +364,8 @@ def main_gsp(args):
     ev = {k: [] for k in op_names + ["exchange"]}
 
     # the step as a list of (name, launch, input index into (X, dY, Z, dO) or None, output index or None)
-    def op_list():
+    def op_list(ins=None, outs=outs):
+        X, dY, Z, dO = ins if ins is not None else (X_, dY_, Z_, dO_)
         L = [("gspmm_fwd", lambda: part.gspmm(X, gsp.NORM_BOTH, out=outs[0], stream=stream), 0, 0),
              ("gspmm_rev", lambda: part.gspmm(dY, gsp.NORM_BOTH, out=outs[1], reverse=True, stream=stream), 1, 1)]
         if fused:   # A5-A7 in one pass per destination row; s ends up holding alpha, as below
@@ -403,7 +405,7 @@ def main_gsp(args):
     # 1-GPU box): the host-staged exchange() after the last op.
     overlap = P > 1 and backend == "nccl"
 
-    def issue_collective(name, i_out, pending):
+    def issue_collective(name, i_out, pending, outs=outs):
         if not overlap:
             return
         if name == "gspmm_weighted_rev":
@@ -500,36 +502,47 @@ def main_gsp(args):
         del ref1, ref2, ref3, ref4, sf, Xf, dYf, Zf, dOf
 
     # ---------------------------------------------------------------- e2e
+    # The same step through the C ABI with HOST buffers: every step copies its four
+    # input tables from pinned host memory (H2D engine) and reads its four outputs
+    # back (D2H engine), inside the timed region.  Steps are pipelined the way a
+    # stream of batches runs: two device buffer sets, so step k+1's inputs upload
+    # while step k computes and step k's outputs download while step k+1 computes;
+    # each op waits only for its own input, each output leaves as soon as it is
+    # final.  No L2 flush between steps: each step's inputs (4 x 59.6 MB tables +
+    # 3.67 GB of alpha) exceed the 126 MB L2.  gloo ranks (validation): no e2e.
     e2e = None
-    if not args.no_e2e and not args.profile:
+    if not args.no_e2e and not args.profile and (P == 1 or overlap):
         hin = [torch.empty((ncols, F), dtype=torch.float32).pin_memory() for _ in range(4)]
         for h, d in zip(hin, (X, dY, Z, dO)):
             h.copy_(d.cpu())
-        hout = [torch.empty((R, F), dtype=torch.float32).pin_memory() for _ in range(4)]
-        dins = (X, dY, Z, dO)
-
+        sets = [((X, dY, Z, dO), outs),
+                (tuple(torch.empty_like(t) for t in (X, dY, Z, dO)), [torch.empty_like(o) for o in outs])]
+        ops_of = [op_list(*sets[0]), op_list(*sets[1])]
+        hout = [[torch.empty((R, F), dtype=torch.float32).pin_memory() for _ in range(4)] for _ in range(2)]
         h2d = torch.cuda.Stream()
         d2h = torch.cuda.Stream()
+        in_free, out_free = [None, None], [None, None]
 
-        def e2e_step(start_event):
-            # inputs stream in on the H2D engine in the order the ops consume them; each
-            # output streams back on the D2H engine as soon as its op (or exchange) is done
-            h2d.wait_event(start_event)
-            d2h.wait_event(start_event)
+        def e2e_step(k):
+            j = k % 2
+            ins, outs_j = sets[j]
+            if in_free[j] is not None:          # step k-2 is done reading this input set
+                h2d.wait_event(in_free[j])
             ready = []
             with torch.cuda.stream(h2d):
-                for h, d in zip(hin, dins):
+                for h, d in zip(hin, ins):
                     d.copy_(h, non_blocking=True)
                     e = torch.cuda.Event()
                     e.record(h2d)
                     ready.append(e)
-            done = []
-            pending = []
-            for name, fn, i_in, i_out in OPS:
+            if out_free[j] is not None:         # step k-2's outputs have left this set
+                stream.wait_event(out_free[j])
+            done, pending = [], []
+            for name, fn, i_in, i_out in ops_of[j]:
                 if i_in is not None:
                     stream.wait_event(ready[i_in])
                 fn()
-                issue_collective(name, i_out, pending)
+                issue_collective(name, i_out, pending, outs_j)
                 if i_out is not None and P == 1:
                     e = torch.cuda.Event()
                     e.record(stream)
@@ -538,38 +551,47 @@ def main_gsp(args):
                 finish_exchange(pending)
                 e = torch.cuda.Event()
                 e.record(stream)
-                done = [(e, k) for k in range(4)]
+                done = [(e, i) for i in range(4)]
+            f = torch.cuda.Event()
+            f.record(stream)
+            in_free[j] = f
             with torch.cuda.stream(d2h):
-                for e, k in done:
+                for e, i in done:
                     d2h.wait_event(e)
-                    hout[k].copy_(outs[k], non_blocking=True)
-            fin = torch.cuda.Event()
-            fin.record(d2h)
-            stream.wait_event(fin)
-            stream.wait_stream(h2d)
+                    hout[j][i].copy_(outs_j[i], non_blocking=True)
+            g = torch.cuda.Event()
+            g.record(d2h)
+            out_free[j] = g
 
-        for _ in range(2):
-            st = torch.cuda.Event()
-            st.record(stream)
-            e2e_step(st)
+        for k in range(2):
+            e2e_step(k)
         torch.cuda.synchronize()
-        e_ms = []
-        for _ in range(max(3, args.steps // 2)):
-            flush.fill_(1.0)
-            a0 = torch.cuda.Event(enable_timing=True)
-            a1 = torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            e2e_step(a0)
-            a1.record(stream)
-            torch.cuda.synchronize()
-            e_ms.append(a0.elapsed_time(a1))
-        t_e2e = sum(e_ms) / len(e_ms)
+        if P > 1:
+            dist.barrier()
+        K = max(4, args.steps)
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        h2d.wait_event(a0)
+        d2h.wait_event(a0)
+        for k in range(K):
+            e2e_step(k)
+        stream.wait_stream(h2d)
+        stream.wait_stream(d2h)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        t_e2e = a0.elapsed_time(a1) / K
         if P > 1:
             t_e2e = allreduce_max(t_e2e)
+        # the host copies hold what the device computed
+        assert torch.equal(hout[(K - 1) % 2][0], sets[(K - 1) % 2][1][0].cpu())
         e2e = {"value": round(N_OPS * E / (t_e2e * 1e-3) / 1e9, 4), "unit": "GE/s",
-               "ms_per_step": round(t_e2e, 4),
+               "ms_per_step": round(t_e2e, 4), "steps": K,
                "h2d_bytes_per_step": int(sum(h.numel() * 4 for h in hin)),
-               "d2h_bytes_per_step": int(sum(h.numel() * 4 for h in hout))}
+               "d2h_bytes_per_step": int(sum(h.numel() * 4 for h in hout[0])),
+               "how": "pinned host buffers, H2D / D2H engines overlapped with the kernels and pipelined across "
+                      "steps (two device buffer sets); no L2 flush (per-step inputs exceed L2)"}
+        del sets, ops_of
 
     # ------------------------- launch-bound configs (BASELINE configs[0], [1])
     latency = None
