@@ -270,7 +270,7 @@ bool gat_fused_supported(const GatArgs &a) {
 static int64_t gat_score_bytes() {
     static const int64_t v = [] {
         const char *e = getenv("GSP_GAT_SMEM_KB");
-        return (e ? atoll(e) : int64_t(6)) << 10;   // 6 KB: 3.26 -> 3.02 ms on Reddit 8x8; 11 KB: 4.2 ms (L1 squeezed)
+        return (e ? atoll(e) : int64_t(7)) << 10;   // 7 KB (224 edges at H = 8): 3.26 -> 2.93 ms on Reddit 8x8; 11 KB: 4.2 ms (L1 squeezed)
     }();
     return v;
 }
