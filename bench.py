@@ -649,6 +649,9 @@ def main_gsp(args):
         ms_e = time_op(lambda: part.gspmm_e(s, gsp.REDUCE_SUM, out=hout, stream=stream))
         ms_ve = time_op(lambda: part.gsddmm_ve(Z[:, :H], dal, gsp.OP_ADD, gsp.SIDE_SRC, out=alpha2, stream=stream))
         ms_sbw = time_op(lambda: part.edge_softmax_backward(s, dal, out=dal, stream=stream))
+        # NEXT-1 fused: gSDDMM(dO, Z) + softmax backward in one pass (vs the two calls)
+        ms_gbw = time_op(lambda: part.gat_backward_scores(dO, Z, s, out=alpha2, stream=stream))
+        ms_gbw_sep = time_op(lambda: part.gsddmm(dO, Z, out=alpha2, stream=stream)) + ms_sbw
         sep = sum((outside if fused else avg)[k] for k in ("gsddmm", "edge_softmax", "gspmm_weighted_fwd"))
         next_rows = {
             "gat_forward_fused": {"row": "NEXT-2", "ms": round(ms_gat, 4), "in_step": fused,
@@ -663,6 +666,8 @@ def main_gsp(args):
             "gsddmm_ve_add_src": {"row": "NEXT-3", "ms": round(ms_ve, 4),
                                   "GB_s": round((2 * Eloc * H * 4 + Eloc * 4 + (Vloc + 1) * 8 + V * H * 4)
                                                 / (ms_ve * 1e-3) / 1e9, 1)},
+            "gat_backward_scores_fused": {"row": "NEXT-1", "ms": round(ms_gbw, 4),
+                                          "vs_gsddmm_plus_softmax_backward_ms": round(ms_gbw_sep, 4)},
             "edge_softmax_backward": {"row": "NEXT-1", "ms": round(ms_sbw, 4),
                                       "GB_s": round(alg_bytes("edge_softmax", Vloc, Eloc, F, H) * 1.5 / (ms_sbw * 1e-3) / 1e9, 1)},
         }

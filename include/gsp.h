@@ -197,6 +197,24 @@ gsp_status gsp_edge_softmax_backward(const gsp_graph *g, const gsp_tensor *alpha
 gsp_status gsp_gat_forward(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *Y, const gsp_tensor *Vt,
                            gsp_tensor *alpha, gsp_tensor *out, gsp_stream stream);
 
+/* Fused GAT backward scores ("Backward
+ * Computation"; P:1458-1518 the state tensor alpha): the gradient of the
+ * attention scores of one GAT layer out = gspmm_weighted(Vt, alpha), in one
+ * pass per destination row:
+ *   dalpha[j,h] = <dOut[v, head h], Vt[u_j, head h]>          (as gsp_gsddmm(dOut, Vt))
+ *   ds[j,h]     = alpha[j,h] (dalpha[j,h] - sum_{j' in row v} alpha[j',h] dalpha[j',h])
+ *                                                              (as gsp_edge_softmax_backward)
+ * dOut, Vt [ncols, F] (dOut by destination, like gsddmm's X; partitions: the
+ * padded tables), alpha, ds [E, H] by edge ID.  Fused when F = 8 H, H in
+ * {2, 4, 8, 16}, alpha->ld = ds->ld = H and 32-byte aligned tables; else the
+ * two kernels in sequence.  The rest of the layer's backward: dZ through the
+ * aggregation = gsp_gspmm_weighted(dOut, alpha, reverse = 1); the score
+ * inputs' gradients = gsp_gspmm_weighted(Y, ds) and (X, ds, reverse = 1).
+ * Errors: NULL, ARG, SHAPE (1 <= H <= 16, F % H == 0), ALIAS (ds overlapping
+ * any input), CUDA. */
+gsp_status gsp_gat_backward_scores(const gsp_graph *g, const gsp_tensor *dOut, const gsp_tensor *Vt,
+                                   const gsp_tensor *alpha, gsp_tensor *ds, gsp_stream stream);
+
 /* ---------------------------------------- Table 1 surface (NEXT-3, §8(f)) */
 enum { GSP_REDUCE_SUM = 0, GSP_REDUCE_MIN = 1, GSP_REDUCE_MAX = 2 };
 enum { GSP_OP_ADD = 0, GSP_OP_SUB = 1, GSP_OP_MUL = 2, GSP_OP_DIV = 3 };

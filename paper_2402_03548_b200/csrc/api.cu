@@ -621,6 +621,61 @@ gsp_status gsp_gat_forward(const gsp_graph *g, const gsp_tensor *X, const gsp_te
     return GSP_OK;
 }
 
+gsp_status gsp_gat_backward_scores(const gsp_graph *g, const gsp_tensor *dOut, const gsp_tensor *Vt,
+                                   const gsp_tensor *alpha, gsp_tensor *ds, gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    const gsp::DevStructure &S = g->fwd;
+    if (!S.present) return fail(GSP_ERR_ARG, "gat_backward_scores needs the fwd structure (not a reverse partition)");
+    if (!dOut || !Vt || !alpha || !ds) return fail(GSP_ERR_NULL, "dOut/Vt/alpha/ds is NULL");
+    if ((st = check_tensor(g, alpha, "alpha", g->E, -1)) != GSP_OK) return st;
+    const int64_t H = alpha->cols;
+    if (H < 1 || H > 16) return fail(GSP_ERR_SHAPE, "alpha must have 1 <= H <= 16 columns (heads)");
+    if ((st = check_tensor(g, ds, "ds", g->E, H)) != GSP_OK) return st;
+    if ((st = check_tensor(g, dOut, "dOut", S.ncols, -1)) != GSP_OK) return st;
+    if ((st = check_tensor(g, Vt, "Vt", S.ncols, dOut->cols)) != GSP_OK) return st;
+    if (dOut->cols % H != 0) return fail(GSP_ERR_SHAPE, "dOut.cols must be a multiple of H");
+    if (overlaps(ds, alpha) || overlaps(ds, dOut) || overlaps(ds, Vt))
+        return fail(GSP_ERR_ALIAS, "ds overlaps alpha, dOut or Vt");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    cudaStream_t cs = (cudaStream_t)stream;
+    gsp::GatArgs ga{};
+    ga.off = S.off; ga.col = S.col; ga.order = S.order; ga.task = S.task; ga.nrows = S.nrows; ga.n_heavy = S.n_heavy;
+    ga.row_base = g->row_base;
+    ga.X = static_cast<const float *>(dOut->data); ga.ldx = dOut->ld;
+    ga.Y = ga.X; ga.ldy = dOut->ld;
+    ga.Vt = static_cast<const float *>(Vt->data); ga.ldv = Vt->ld;
+    ga.alpha = static_cast<float *>(alpha->data);   // read only
+    ga.out = static_cast<float *>(ds->data); ga.ldo = ds->ld;
+    ga.H = H;
+    const bool fused = dOut->cols == 8 * H && alpha->ld == H && ds->ld == H && H != 1 && gsp::gat_fused_supported(ga);
+    cudaError_t e;
+    if (fused) {
+        e = gsp::launch_gat_bwd(ga, cs);
+    } else {
+        // any other shape: gSDDMM into ds (as dalpha), then the softmax backward in place
+        gsp::SddmmArgs sa{};
+        sa.off = S.off; sa.col = S.col; sa.order = S.order; sa.task = S.task; sa.nrows = S.nrows; sa.n_heavy = S.n_heavy;
+        sa.row_base = g->row_base;
+        sa.X = ga.X; sa.ldx = dOut->ld; sa.Y = ga.Vt; sa.ldy = Vt->ld;
+        sa.out = ga.out; sa.ldo = ds->ld; sa.H = H; sa.Fh = dOut->cols / H;
+        e = sa.Fh > 0 ? gsp::launch_sddmm(sa, cs)
+                      : cudaMemset2DAsync(ds->data, (size_t)ds->ld * 4, 0, (size_t)H * 4, (size_t)g->E, cs);
+        if (e == cudaSuccess) {
+            gsp::SoftmaxBwdArgs a{};
+            a.off = S.off; a.order = S.order; a.task = S.task; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+            a.alpha = ga.alpha; a.lda = alpha->ld;
+            a.dalpha = ga.out; a.ldd = ds->ld;
+            a.out = ga.out; a.ldo = ds->ld;
+            a.H = H;
+            e = gsp::launch_softmax_bwd(a, cs);
+        }
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "gat_backward_scores launch");
+    return GSP_OK;
+}
+
 // ------------------------------------------------ NEXT-3: Table 1 surface
 gsp_status gsp_gspmm_reduce(const gsp_graph *g, const gsp_tensor *X, int reduce, gsp_tensor *out, int reverse,
                             gsp_stream stream) {

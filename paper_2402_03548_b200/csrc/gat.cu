@@ -257,6 +257,140 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
     }
 }
 
+
+// ================================================ fused GAT backward scores
+// NEXT-1 ("Backward Computation"): the score
+// gradient of one GAT layer in one pass per destination row v, one lane per
+// head (Fh = 8 features per lane), a = GatArgs with X = dOut (destination
+// side), Vt = the aggregated table, alpha = the forward state, out = ds:
+//   dalpha[j,h] = <dOut[v,h], Vt[u_j,h]>                  (gSDDMM, C6)
+//   ds[j,h]     = alpha[j,h] (dalpha[j,h] - c_h),  c_h = sum_j alpha[j,h] dalpha[j,h]   (C9)
+// Phase 1 gathers Vt rows, computes dalpha and the per-head row sum c (tile
+// sums folded with Kahan compensation); dalpha of the first `cap` edges of the
+// warp slice stays in shared memory, the rest is parked in ds itself.  Phase 2
+// (after c is complete, across warps for CTA-split rows) streams
+// ds = alpha (dalpha - c).
+template <int LPE>
+__global__ void __launch_bounds__(kThreads, 2) gat_bwd_kernel(const GatArgs a) {
+    constexpr int VEC = 8;
+    constexpr int G = 32 / LPE;
+    constexpr int PER = LPE;
+    constexpr int U = PER >= 8 ? 8 : PER;
+    __shared__ __align__(16) int s_col[kWarps][32];
+    __shared__ float s_c[kWarps][32];
+    extern __shared__ __align__(16) float s_sc[];   // [kWarps][cap][H] dalpha
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPE, h = lane % LPE;
+    const int H = LPE;
+
+    int64_t row, b, e;
+    bool heavy;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    const Pol pol = make_pol();
+    const int64_t cap = a.sc_cap;
+    float *wsc = s_sc + (int64_t)warp * cap * LPE;
+    const float *al = a.alpha;
+
+    Vec<VEC> xv;
+    ld_keep(xv, a.X + (a.row_base + row) * a.ldx + h * VEC, pol.stream);
+    const char *vl = reinterpret_cast<const char *>(a.Vt + h * VEC);
+    const uint32_t ldvb = (uint32_t)(a.ldv * 4);
+
+    float c = 0.f, cc = 0.f, ct = 0.f;   // Kahan running sum of alpha * dalpha, tile sum
+    int ntile = 0;
+    auto load_col = [&](int64_t tb) { return tb + lane < e ? ld_stream_i32(a.col + tb + lane, pol.stream) : 0; };
+    int c1 = load_col(b), c2 = load_col(b + 32);
+    for (int64_t base = b; base < e; base += 32) {
+        const int n = (int)(e - base < 32 ? e - base : 32);
+        s_col[warp][(lane % G) * PER + lane / G] = c1;
+        c1 = c2;
+        c2 = load_col(base + 64);
+        __syncwarp();
+        const int *gp = &s_col[warp][g * PER];
+        const bool in_smem = base - b < cap;
+        float *db = in_smem ? wsc + (base - b + g) * H + h : a.out + (base + g) * H + h;
+        const float *ab = al + (base + g) * H + h;
+        const int mcount = n == 32 ? PER : (n > g ? (n - g + G - 1) / G : 0);
+#pragma unroll 1
+        for (int i = 0; i < mcount; i += U) {
+            Vec<VEC> y[U];
+            float av[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (i + u < mcount) {
+                    ld_keep(y[u], reinterpret_cast<const float *>(vl + (uint64_t)(uint32_t)gp[i + u] * ldvb), pol.keep);
+                    av[u] = ld_f32(ab + (int64_t)(G * (i + u)) * H, pol.keep);   // re-read in phase 2
+                } else {
+                    vzero(y[u]);
+                    av[u] = 0.f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+                for (int t = 0; t < VEC; t += 2) {
+                    s0 = fmaf(xv.v[t], y[u].v[t], s0);
+                    s1 = fmaf(xv.v[t + 1], y[u].v[t + 1], s1);
+                }
+                const float d = s0 + s1;
+                if (i + u < mcount) db[(int64_t)(G * (i + u)) * H] = d;
+                ct = fmaf(av[u], d, ct);
+            }
+        }
+        __syncwarp();
+        if (++ntile == kFoldTiles || base + 32 >= e) {   // Kahan fold of the tile sum
+            ntile = 0;
+            const float y2 = ct - cc, t2 = c + y2;
+            cc = (t2 - c) - y2;
+            c = t2;
+            ct = 0.f;
+        }
+    }
+    c -= cc;
+#pragma unroll
+    for (int o = LPE; o < 32; o <<= 1) c += __shfl_xor_sync(kFull, c, o);   // the G groups of head h
+    if (heavy) {   // the CTA's warps hold slices of one row: sum in warp order
+        if (g == 0) s_c[warp][h] = c;
+        __syncthreads();
+        c = 0.f;
+        for (int w = 0; w < kWarps; w++) c += s_c[w][h];
+    }
+    // phase 2: ds = alpha (dalpha - c) over the warp's slice; element i has head i % H
+    __syncwarp();
+    const int64_t lo = b * H, hi = e * H, mid = min(hi, lo + cap * H);
+    if (H % 4 == 0) {
+        float ch[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) ch[t] = __shfl_sync(kFull, c, (lane * 4 + t) % H);
+        constexpr int NU = 4;   // loads in flight per lane
+        for (int64_t i0 = lo + (int64_t)lane * 4; i0 < hi; i0 += 128 * NU) {
+            float4 d[NU], av[NU];
+#pragma unroll
+            for (int k = 0; k < NU; k++) {
+                const int64_t i = i0 + 128 * k;
+                if (i < hi) {
+                    av[k] = ld_f4(al + i, pol.stream);
+                    d[k] = i < mid ? *reinterpret_cast<const float4 *>(wsc + (i - lo)) : ld_f4(a.out + i, pol.stream);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NU; k++) {
+                const int64_t i = i0 + 128 * k;
+                if (i < hi)
+                    st_stream_f4(a.out + i, make_float4(av[k].x * (d[k].x - ch[0]), av[k].y * (d[k].y - ch[1]),
+                                                        av[k].z * (d[k].z - ch[2]), av[k].w * (d[k].w - ch[3])),
+                                 pol.stream);
+            }
+        }
+    } else {
+        const float chh = __shfl_sync(kFull, c, lane % H);
+        for (int64_t i = lo + lane; i < hi; i += 32) {
+            const float d = i < mid ? wsc[i - lo] : ld_f32(a.out + i, pol.stream);
+            st_stream_f32(a.out + i, ld_f32(al + i, pol.stream) * (d - chh), pol.stream);
+        }
+    }
+}
 }  // namespace
 
 bool gat_fused_supported(const GatArgs &a) {
@@ -306,6 +440,35 @@ cudaError_t launch_gat_fused(const GatArgs &a, cudaStream_t s) {
         default: return same ? launch_gat_h<32, true>(a, grid, s) : launch_gat_h<32, false>(a, grid, s);
     }
 #undef GSP_GAT_CASE
+}
+
+template <int HH>
+cudaError_t launch_gat_bwd_h(GatArgs a, dim3 grid, cudaStream_t s) {
+    a.sc_cap = (gat_score_bytes() / (4 * HH)) & ~int64_t(31);
+    const size_t dyn = (size_t)(kWarps * a.sc_cap * HH * 4);
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 64 || !attr[dev]) {
+        e = cudaFuncSetAttribute(gat_bwd_kernel<HH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (e != cudaSuccess) return e;
+        if (dev < 64) attr[dev] = true;
+    }
+    gat_bwd_kernel<HH><<<grid, kThreads, dyn, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gat_bwd(const GatArgs &a, cudaStream_t s) {
+    if (a.nrows == 0) return cudaSuccess;
+    const dim3 grid = row_grid(a.nrows, a.n_heavy, 1);
+    switch (a.H) {
+        case 2: return launch_gat_bwd_h<2>(a, grid, s);
+        case 4: return launch_gat_bwd_h<4>(a, grid, s);
+        case 8: return launch_gat_bwd_h<8>(a, grid, s);
+        case 16: return launch_gat_bwd_h<16>(a, grid, s);
+        default: return launch_gat_bwd_h<32>(a, grid, s);
+    }
 }
 
 }  // namespace gsp

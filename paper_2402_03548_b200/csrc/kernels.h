@@ -101,6 +101,8 @@ struct GatArgs {
 };
 bool gat_fused_supported(const GatArgs &a);
 cudaError_t launch_gat_fused(const GatArgs &a, cudaStream_t s);
+// fused GAT backward scores (NEXT-1): X = dOut (destination side), Vt, alpha (read), out = ds [E, H]
+cudaError_t launch_gat_bwd(const GatArgs &a, cudaStream_t s);
 
 // NEXT-3 (Table 1 surface): gSpMMe / gSpMMeid and gSDDMMve.
 struct SpmmEArgs {

@@ -30,7 +30,7 @@ STATUS = {0: "GSP_OK", 1: "GSP_ERR_NULL", 2: "GSP_ERR_ARG", 3: "GSP_ERR_VERTEX_R
 # the exported C symbols (include/gsp.h), checked by tests/test_abi.py
 SYMBOLS = ["gsp_graph_create", "gsp_graph_destroy", "gsp_graph_info", "gsp_graph_export", "gsp_gspmm",
            "gsp_gspmm_weighted", "gsp_gsddmm", "gsp_edge_softmax", "gsp_edge_softmax_backward",
-           "gsp_gat_forward", "gsp_gspmm_reduce", "gsp_gspmm_e", "gsp_gsddmm_ve", "gsp_partition_bounds", "gsp_graph_partition",
+           "gsp_gat_forward", "gsp_gat_backward_scores", "gsp_gspmm_reduce", "gsp_gspmm_e", "gsp_gsddmm_ve", "gsp_partition_bounds", "gsp_graph_partition",
            "gsp_partition_info", "gsp_status_string", "gsp_last_error_detail", "gsp_version"]
 
 
@@ -65,6 +65,7 @@ def _load():
         "gsp_edge_softmax": ([p, T, T, p], ci),
         "gsp_edge_softmax_backward": ([p, T, T, T, p], ci),
         "gsp_gat_forward": ([p, T, T, T, T, T, p], ci),
+        "gsp_gat_backward_scores": ([p, T, T, T, T, p], ci),
         "gsp_gspmm_reduce": ([p, T, ci, T, ci, p], ci),
         "gsp_gspmm_e": ([p, T, ci, T, ci, p], ci),
         "gsp_gsddmm_ve": ([p, T, T, ci, ci, T, p], ci),
@@ -245,6 +246,19 @@ def _gat_forward(self, X, Y, Vt, H, alpha=None, out=None, stream=None):
 
 
 Graph.gat_forward = _gat_forward
+
+
+def _gat_backward_scores(self, dOut, Vt, alpha, out=None, stream=None):
+    """ds = edge_softmax_backward(alpha, gsddmm(dOut, Vt)) -- fused (NEXT-1)."""
+    if out is None:
+        out = self._alloc(self.E, alpha.shape[1], alpha)
+    dd, dv, da, do = _desc(dOut), _desc(Vt), _desc(alpha), _desc(out)
+    _check(lib.gsp_gat_backward_scores(self._h, ctypes.byref(dd), ctypes.byref(dv), ctypes.byref(da),
+                                       ctypes.byref(do), _stream(stream, alpha.device)))
+    return out
+
+
+Graph.gat_backward_scores = _gat_backward_scores
 
 
 def _gspmm_reduce(self, X, reduce, out=None, reverse=False, stream=None):

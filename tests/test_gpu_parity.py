@@ -635,3 +635,52 @@ def test_cuda_graph_capture_replay(gsp):
     torch.cuda.synchronize()
     for a, b in zip((o1, o2, o3, s), ref):
         assert torch.equal(a, b)
+
+
+# ------------------------------------------- NEXT-1: fused GAT backward scores
+def _gat_bwd_check(gsp, V, src, dst, H, Fh, seed=0):
+    """ds = C9(alpha, C6(dOut, Vt)) composed from the oracle.  Bound 1e-5 (T + 1),
+    T = C9's sum|terms| plus the propagation of dalpha's own fp32 dot error:
+    alpha_j T6_j + alpha_j sum_j' alpha_j' T6_j' (T6 = C6's sum|terms|)."""
+    G, og = graph_pair(gsp, V, src, dst)
+    F = H * Fh
+    dOh = datagen.uniform(seed + 1, V, F)
+    Vh = datagen.uniform(seed + 2, V, F)
+    ah = og.edge_softmax(datagen.uniform(seed + 3, og.E, H, lo=-4, hi=4)).astype(np.float32)
+    d64, T6 = og.gsddmm(dOh, Vh, H)
+    ref, T9 = og.edge_softmax_backward(ah, d64.astype(np.float32))
+    rid = np.repeat(np.arange(V), np.diff(og.fwd_off))
+    S = np.zeros((V, H))
+    np.add.at(S, rid, ah * T6)
+    T = T9 + ah * T6 + ah * S[rid]
+    ds = G.gat_backward_scores(dev(dOh), dev(Vh), dev(ah))
+    assert_within(ds.cpu().numpy(), ref, T, f"gat bwd H{H} Fh{Fh}")
+    return G, og
+
+
+@pytest.mark.parametrize("H,Fh", [(8, 8), (4, 8), (2, 8), (16, 8), (1, 8), (3, 5), (8, 4)])
+def test_gat_backward_scores_random(gsp, H, Fh):
+    for seed in range(2):
+        rng = np.random.default_rng(seed + 10 * H + Fh)
+        V = int(rng.integers(50, 2500))
+        E = int(rng.integers(0, 30000))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed == 0 else datagen.skewed_multigraph(V, E, seed))
+        _gat_bwd_check(gsp, V, src, dst, H, Fh, seed)
+
+
+def test_gat_backward_scores_heavy_rows_pubmed_and_errors(gsp):
+    V, E = 3000, 120_000   # CTA-split hub rows (> 2048 edges) and rows past the 224-edge score block
+    src, dst = datagen.skewed_multigraph(V, E, 4, alpha=1.6)
+    G, og = _gat_bwd_check(gsp, V, src, dst, 8, 8, seed=4)
+    assert np.diff(og.fwd_off).max() > 2048
+    cfg = datagen.CONFIGS["pubmed"]
+    Vp, sp, dp = datagen.make_graph(cfg)
+    _gat_bwd_check(gsp, Vp, sp, dp, cfg.H, cfg.Fh, seed=5)
+    a = torch.rand((og.E, 8), device="cuda")
+    X = torch.rand((V, 64), device="cuda")
+    with pytest.raises(gsp.GspError) as ei:
+        G.gat_backward_scores(X, X, a, out=a)
+    assert ei.value.name == "GSP_ERR_ALIAS"
+    with pytest.raises(gsp.GspError) as ei:
+        G.gat_backward_scores(X[:, :60], X[:, :60], torch.rand((og.E, 8), device="cuda"))
+    assert ei.value.name == "GSP_ERR_SHAPE"

@@ -48,6 +48,7 @@ ops = {
     "wfwd": lambda: G.gspmm_weighted(Z, s, out=outg),
     "wrev": lambda: G.gspmm_weighted(Z, s, out=outg, reverse=True),
     "gat_fused": lambda: G.gat_forward(Z, Z, Z, H, alpha=s, out=outg),
+    "gat_bwd": lambda: G.gat_backward_scores(Z, Z, s, out=s2),
     "softmax_bwd": lambda: G.edge_softmax_backward(s, s2, out=s2),
     "e_sum": lambda: G.gspmm_e(s, 0, out=outh),
     "e_sum_rev": lambda: G.gspmm_e(s, 0, out=outh, reverse=True),

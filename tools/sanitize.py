@@ -17,7 +17,8 @@ def run(V, src, dst, F=64, H=8):
     g.gspmm_weighted(X, s)
     g.gspmm_weighted(X, s, reverse=True)
     g.edge_softmax_backward(s, s.clone())
-    g.gat_forward(X, X, X, H)
+    a, _ = g.gat_forward(X, X, X, H)
+    g.gat_backward_scores(X, X, a)
     g.gspmm_e(s, 0)
     g.gspmm_e(s, 2, reverse=True)
     g.gsddmm_ve(X[:, :H], s, 0, 1)
