@@ -122,6 +122,34 @@ def test_reddit_gat_forward_fused_sampled(reddit):
     within(out[torch.from_numpy(rows).cuda()].cpu().numpy(), o_ref[rows], T[rows], scale=2e-5)
 
 
+def test_reddit_gat_backward_scores_sampled(reddit):
+    """The fused GAT backward scores (NEXT-1) at full size, as bench.py's next_rows
+    calls it (dOut, Z, alpha of the forward, H = 8 x 8): ds of sampled rows against
+    the oracle composition C9 o C6 on the sub-graph of those rows' in-edges (a
+    row's ds depends only on its own edges).  Bound as the small-size test."""
+    cfg, G, og = reddit
+    H, F = cfg.H, cfg.H * cfg.Fh
+    rows = sample_rows(og.fwd_off, 93)
+    eids = og.row_edges(rows)
+    sub = oracle.Graph(og.V, og.fwd_col[eids].astype(np.int64),
+                       np.repeat(rows, og.fwd_off[rows + 1] - og.fwd_off[rows]))
+    Zh = datagen.uniform(21, og.V, F)
+    dOh = datagen.uniform(22, og.V, F)
+    Z, dO = dev(Zh), dev(dOh)
+    alpha, _ = G.gat_forward(Z, Z, Z, H)
+    ds = G.gat_backward_scores(dO, Z, alpha)
+    e = torch.from_numpy(eids).cuda()
+    ah = alpha[e].cpu().numpy()
+    got = ds[e].cpu().numpy()
+    del alpha, ds
+    d64, T6 = sub.gsddmm(dOh, Zh, H)
+    ref, T9 = sub.edge_softmax_backward(ah, d64.astype(np.float32))
+    rid = np.repeat(np.arange(len(rows)), og.fwd_off[rows + 1] - og.fwd_off[rows])
+    S = np.zeros((len(rows), H))
+    np.add.at(S, rid, ah * T6)
+    within(got, ref, T9 + ah * T6 + ah * S[rid])
+
+
 def test_products_gspmm_sampled():
     import paper_2402_03548_b200 as gsp
     cfg = datagen.CONFIGS["products"]
