@@ -234,36 +234,17 @@ def cpu_oracle_bench(V, src, dst, cfg, target_edges, steps=1, warmup=0):
 
 # ------------------------------------------------------------------ GPU arm
 def small_config_latency(gsp, torch):
-    """Cora GCN fwd+bwd (F=16) and Pubmed GAT chain (8x8): microseconds per step,
-    eager vs the same calls captured in one CUDA graph (the launch-bound regime of
-    P:1632-1688)."""
+    """Cora GCN fwd+bwd (F=16) and the Pubmed GAT forward (8x8, as three calls and
+    as the fused kernel): microseconds per step, eager vs the same calls captured
+    in one CUDA graph (the launch-bound regime of P:1632-1688)."""
     res = {}
     st = torch.cuda.Stream()
-    for name in ("cora", "pubmed"):
-        cfg = datagen.CONFIGS[name]
-        V, src, dst = datagen.make_graph(cfg)
-        G = gsp.Graph(V, src, dst, device=torch.cuda.current_device())
-        F = cfg.F
-        X = torch.from_numpy(datagen.uniform(1, V, F)).cuda()
-        o1 = torch.empty((V, F), device="cuda")
-        o2 = torch.empty((V, F), device="cuda")
-        if name == "cora":
-            def stepf():
-                G.gspmm(X, gsp.NORM_BOTH, out=o1, stream=st)
-                G.gspmm(o1, gsp.NORM_BOTH, out=o2, reverse=True, stream=st)
-            n_ops = 2
-        else:
-            s = torch.empty((G.E, cfg.H), device="cuda")
-            def stepf():
-                G.gsddmm(X, X, out=s, stream=st)
-                G.edge_softmax(s, out=s, stream=st)
-                G.gspmm_weighted(X, s, out=o1, stream=st)
-            n_ops = 3
+
+    def timed(stepf, reps=200):
         with torch.cuda.stream(st):
             for _ in range(5):
                 stepf()
         torch.cuda.synchronize()
-        reps = 200
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(st)
         with torch.cuda.stream(st):
@@ -284,12 +265,38 @@ def small_config_latency(gsp, torch):
                 gr.replay()
         a1.record(st)
         torch.cuda.synchronize()
-        graph = a0.elapsed_time(a1) * 1e3 / reps
-        res[name] = {"ops": "gspmm fwd+rev (BOTH), F=16" if name == "cora" else "gsddmm+softmax+weighted, 8x8",
-                     "n_kernels": n_ops, "eager_us_per_step": round(eager, 2), "cuda_graph_us_per_step": round(graph, 2),
-                     "V": V, "E": int(G.E)}
-    return res
+        return round(eager, 2), round(a0.elapsed_time(a1) * 1e3 / reps, 2)
 
+    for name in ("cora", "pubmed"):
+        cfg = datagen.CONFIGS[name]
+        V, src, dst = datagen.make_graph(cfg)
+        G = gsp.Graph(V, src, dst, device=torch.cuda.current_device())
+        F = cfg.F
+        X = torch.from_numpy(datagen.uniform(1, V, F)).cuda()
+        o1 = torch.empty((V, F), device="cuda")
+        o2 = torch.empty((V, F), device="cuda")
+        if name == "cora":
+            def stepf():
+                G.gspmm(X, gsp.NORM_BOTH, out=o1, stream=st)
+                G.gspmm(o1, gsp.NORM_BOTH, out=o2, reverse=True, stream=st)
+            eager, graph = timed(stepf)
+            res[name] = {"ops": "gspmm fwd+rev (BOTH), F=16", "n_kernels": 2, "eager_us_per_step": eager,
+                         "cuda_graph_us_per_step": graph, "V": V, "E": int(G.E)}
+        else:
+            s = torch.empty((G.E, cfg.H), device="cuda")
+            def stepf():
+                G.gsddmm(X, X, out=s, stream=st)
+                G.edge_softmax(s, out=s, stream=st)
+                G.gspmm_weighted(X, s, out=o1, stream=st)
+            def fusedf():
+                G.gat_forward(X, X, X, cfg.H, alpha=s, out=o1, stream=st)
+            eager, graph = timed(stepf)
+            feager, fgraph = timed(fusedf)
+            res[name] = {"ops": "GAT forward 8x8: gsddmm+softmax+weighted (3 kernels) / fused (1 kernel)",
+                         "n_kernels": 3, "eager_us_per_step": eager, "cuda_graph_us_per_step": graph,
+                         "fused_eager_us_per_step": feager, "fused_cuda_graph_us_per_step": fgraph,
+                         "V": V, "E": int(G.E)}
+    return res
 
 
 def main_gsp(args):
