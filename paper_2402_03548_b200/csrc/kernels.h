@@ -26,6 +26,7 @@ struct SpmmArgs {
     int64_t ldw;
     int64_t H, Fh;
     int pf;                  // L2 prefetch distance of the edge streams, in 32-edge tiles (0 = off)
+    int out_vec;             // out rows 16-B aligned (ldo % 4 == 0): vector stores, else scalar (set by launch_spmm)
 };
 
 enum SpmmMode { kSpmmScaled = 0, kSpmmWeightedFwd = 1, kSpmmWeightedRev = 2, kSpmmMin = 3, kSpmmMax = 4 };

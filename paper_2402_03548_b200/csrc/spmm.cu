@@ -298,7 +298,14 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
                     Vec<VEC> r;
 #pragma unroll
                     for (int t = 0; t < VEC; t++) r.v[t] = (MM && b == e) ? 0.f : rs * acc[q].v[t];   // empty row -> 0
-                    vstore(a.out + row * a.ldo + f, r, a.F - f);
+                    float *o = a.out + row * a.ldo + f;
+                    if (a.out_vec) {
+                        vstore(o, r, a.F - f);
+                    } else {   // odd output stride: the gathers stay vectorised, the row store is scalar
+#pragma unroll
+                        for (int t = 0; t < VEC; t++)
+                            if (f + t < a.F) o[t] = r.v[t];
+                    }
                 }
             }
         }
@@ -555,9 +562,11 @@ cudaError_t launch_spmm(const SpmmArgs &a_in, int mode, cudaStream_t s) {
     a.pf = prefetch_tiles();
     const bool wmode = mode == kSpmmWeightedFwd || mode == kSpmmWeightedRev;
     if (wmode && a.H > kHMax) return cudaErrorNotSupported;   // api.cu rejects H > 16 first
+    // the gather width depends on X only; an output stride that is not a multiple of 4
+    // (e.g. F = 602 written densely) just makes the row stores scalar
+    a.out_vec = a.ldo % 4 == 0 && aligned(a.out, 16);
     auto ok_vec = [&](int v) {
-        return a.F >= v && a.ldx % v == 0 && a.ldo % 4 == 0 && aligned(a.X, 4 * v) && aligned(a.out, 16) &&
-               (!wmode || a.Fh % v == 0);
+        return a.F >= v && a.ldx % v == 0 && aligned(a.X, 4 * v) && (!wmode || a.Fh % v == 0);
     };
     if (ok_vec(8)) return spmm_dispatch<8, 2>(a, mode, s);
     if (ok_vec(4)) return spmm_dispatch<4, 4>(a, mode, s);

@@ -684,3 +684,29 @@ def test_gat_backward_scores_heavy_rows_pubmed_and_errors(gsp):
     with pytest.raises(gsp.GspError) as ei:
         G.gat_backward_scores(X[:, :60], X[:, :60], torch.rand((og.E, 8), device="cuda"))
     assert ei.value.name == "GSP_ERR_SHAPE"
+
+
+def test_odd_output_stride_keeps_vector_gathers(gsp):
+    """X rows 16-B aligned (vector gathers) but out rows not (ld % 4 != 0: F = 602
+    written densely, odd padding): the row stores fall back to scalar, results
+    unchanged -- gSpMM all norms / directions and weighted fwd / rev."""
+    V, E = 2000, 60_000
+    src, dst = datagen.skewed_multigraph(V, E, 8)
+    G, og = graph_pair(gsp, V, src, dst)
+    for F, ldx, ldo in [(602, 604, 602), (6, 8, 6), (64, 64, 65), (8, 8, 9)]:
+        Xh = datagen.uniform(F + ldo, V, F)
+        X = padded(Xh, ldx)
+        for norm in NORMS:
+            for rev in (0, 1):
+                ref, T = og.gspmm(Xh, norm, rev)
+                out = padded(np.full((V, F), np.nan, np.float32), ldo)
+                G.gspmm(X, norm, out=out, reverse=rev)
+                assert_within(out.cpu().numpy(), ref, T, f"F{F} ldx{ldx} ldo{ldo} n{norm} r{rev}")
+    H, Fh, ldo = 2, 4, 9
+    Xh = datagen.uniform(3, V, H * Fh)
+    wh = datagen.uniform(4, og.E, H, lo=0.0, hi=1.0)
+    for rev in (0, 1):
+        ref, T = og.gspmm_weighted(Xh, wh, bool(rev))
+        out = padded(np.full((V, H * Fh), np.nan, np.float32), ldo)
+        G.gspmm_weighted(dev(Xh), dev(wh), out=out, reverse=rev)
+        assert_within(out.cpu().numpy(), ref, T, f"weighted ldo{ldo} r{rev}")
