@@ -1,6 +1,9 @@
 // gSpMM family: gSpMMv + norm, gSpMMve / gSpMMve^T, min / max, gSpMMe (+ degree / edge scales).
 #include "common.cuh"
 
+#ifndef GSP_MAXCPL4
+#define GSP_MAXCPL4 5   // 128-bit path: max 16-B chunks per lane before the row splits into feature slabs (F = 602: 5 -> one slab, 19.9 ms; 4 -> two slabs, 23.6 ms)
+#endif
 #ifndef GSP_PAIR_LAYOUT
 #define GSP_PAIR_LAYOUT 1
 #endif
@@ -569,7 +572,7 @@ cudaError_t launch_spmm(const SpmmArgs &a_in, int mode, cudaStream_t s) {
         return a.F >= v && a.ldx % v == 0 && aligned(a.X, 4 * v) && (!wmode || a.Fh % v == 0);
     };
     if (ok_vec(8)) return spmm_dispatch<8, 2>(a, mode, s);
-    if (ok_vec(4)) return spmm_dispatch<4, 4>(a, mode, s);
+    if (ok_vec(4)) return spmm_dispatch<4, GSP_MAXCPL4>(a, mode, s);
     return spmm_dispatch<1, 4>(a, mode, s);
 }
 
