@@ -4,6 +4,9 @@
 #ifndef GSP_MAXCPL4
 #define GSP_MAXCPL4 5   // 128-bit path: max 16-B chunks per lane before the row splits into feature slabs (F = 602: 5 -> one slab, 19.9 ms; 4 -> two slabs, 23.6 ms)
 #endif
+#ifndef GSP_TUNE_V4
+#define GSP_TUNE_V4 0   // 1: formula default for the F = 65-128 float4 path (A/B)
+#endif
 #ifndef GSP_PAIR_LAYOUT
 #define GSP_PAIR_LAYOUT 1
 #endif
@@ -519,6 +522,11 @@ cudaError_t spmm_go(const SpmmArgs &a, int mode, int64_t slabs, cudaStream_t s) 
             case 4: return spmm_go_v<VEC, LPE, CPL, 8, 3>(a, mode, slabs, s);
             default: break;
         }
+    }
+    if constexpr (VEC == 4 && LPE == 32 && CPL == 1) {   // rows of 17-32 float4 chunks (e.g. F = 100)
+        // scaled gSpMM on a DRAM-resident table (ogbn-products F = 100): 8 gathers in flight
+        // per lane at 3 CTAs/SM, 9.92 -> 9.18 ms (2 CTAs/SM: 10.6; U = 16: 10.3)
+        if (mode == kSpmmScaled && GSP_TUNE_V4 == 0) return spmm_go_v<VEC, LPE, CPL, 8, 3>(a, mode, slabs, s);
     }
     return spmm_go_v<VEC, LPE, CPL>(a, mode, slabs, s);
 }
