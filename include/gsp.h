@@ -78,7 +78,7 @@ enum {
     GSP_BUILD_EDGE_SCALES = 1u << 2,      /* precompute the per-edge column-side degree scale of the BOTH
                                              norm (4 B per edge per structure; one array when symmetric)
                                              so gsp_gspmm streams it instead of gathering d^-1/2 per edge */
-    GSP_BUILD_L2_PERSIST = 1u << 3        /* opt-in: raise the device's persisting-L2 set-aside
+    GSP_BUILD_L2_PERSIST = 1u << 3,       /* opt-in: raise the device's persisting-L2 set-aside
                                              (cudaLimitPersistingL2CacheSize, device-wide, never lowered)
                                              to min(device maximum, 48 MiB; env GSP_L2_SETASIDE_MB
                                              overrides).  The gathered feature tables are loaded with an
@@ -87,6 +87,14 @@ enum {
                                              GAT forward gain ~5 %, but edge softmax (+10-15 %), its
                                              backward and gSDDMMve lose the L2 capacity they reuse
                                              (DESIGN.md §6).  A failure to set it is ignored (cache hint) */
+    GSP_BUILD_NO_EDGE_IDS = 1u << 4       /* GCN-lean device format ("For GCN, GraphPy need only
+                                             (|V|+|E|)"): no explicit edge-ID array on the device.  With
+                                             GSP_BUILD_SHARE_SYMMETRIC a symmetric graph then stores ONE
+                                             topology (fwd_off + fwd_col) that serves gsp_gspmm in both
+                                             directions; a directed graph stores fwd + rev topology.  The
+                                             edge-ID indirected reverse ops (gsp_gspmm_weighted /
+                                             gsp_gspmm_e with reverse = 1) return GSP_ERR_NO_REVERSE.
+                                             The host structure (gsp_graph_export) is unchanged */
 };
 
 /* gsp_graph_partition flags */
@@ -120,6 +128,15 @@ gsp_status gsp_graph_destroy(gsp_graph *g);
  * scales, schedules); symmetric = 1 if the topology is shared fwd/rev. */
 gsp_status gsp_graph_info(const gsp_graph *g, int64_t *V, int64_t *E, int64_t *device_bytes,
                           int *symmetric);
+
+/* Device bytes of g by kind (any output may be NULL): topology = offsets + column
+ * ids of every stored structure (the paper's |V|+|E| words per structure, P:2012;
+ * a symmetric shared graph stores one), edge_ids = explicit edge-ID arrays
+ * (rev_eid; partitions: the local-rev edge ids), edge_scales = GSP_BUILD_EDGE_SCALES
+ * arrays, vertex_arrays = O(V) degree scales and row schedules.  The four sum to
+ * gsp_graph_info's device_bytes.  Host-only graphs report zeros. */
+gsp_status gsp_graph_memory(const gsp_graph *g, int64_t *topology, int64_t *edge_ids, int64_t *edge_scales,
+                            int64_t *vertex_arrays);
 
 /* Copy the canonical structure into caller-allocated HOST arrays (bit-exact
  * checks).  fwd_off[V+1], fwd_col[E], rev_off[V+1], rev_col[E], rev_eid[E],
@@ -263,7 +280,12 @@ gsp_status gsp_partition_bounds(const gsp_graph *g, int nparts, int reverse, int
  * Compute on a partition graph:
  *  gsp_gspmm(reverse = 0) on a fwd partition / reverse = 1 on a
  *  GSP_PART_REVERSE partition gives rows [b_p, b_p+1) of the full op; on a
- *  symmetric shared graph a fwd partition also serves reverse = 1.
+ *  symmetric shared graph a fwd partition also serves reverse = 1 (its own
+ *  rows).  reverse = 1 on a fwd partition of a DIRECTED graph gives, like the
+ *  weighted reverse below, out [ncols, F]: the contribution of this
+ *  partition's edges to every padded source row, the source-side scale s_src
+ *  already applied; the sum over partitions (one reduce-scatter) is the full
+ *  reverse (adjoint) gSpMMv in the same padded layout.
  *  gsp_gsddmm / gsp_edge_softmax / gsp_gspmm_weighted(reverse=0): fwd
  *  partitions only; the destination-side table of gsddmm is the padded table.
  *  gsp_gspmm_weighted(reverse=1) on a fwd partition: out is [ncols, F], the
@@ -274,6 +296,27 @@ gsp_status gsp_partition_bounds(const gsp_graph *g, int nparts, int reverse, int
  * NO_REVERSE, OOM, CUDA. */
 gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int device, uint32_t flags,
                                gsp_graph **out);
+
+/* Chunked partition for communication / computation overlap:
+ * the rows are cut into Q = nparts * nchunks edge-balanced C8 blocks
+ * (gsp_partition_bounds with Q parts); block q = part * nchunks + chunk is
+ * partition (part, chunk), so rank `part` owns the same rows as with
+ * gsp_graph_partition, split into nchunks consecutive sub-blocks.  The padded
+ * layout is CHUNK-MAJOR: block q sits at slot s(q) = chunk * nparts + part,
+ * R = max_q rows, column v -> s(q(v)) * R + (v - b_q(v)), ncols = Q * R.  For
+ * each chunk c the nparts ranks' [R, F] outputs are therefore the contiguous
+ * rows [c*nparts*R, (c+1)*nparts*R) of the next layer's input: one all-gather
+ * per chunk, issued as soon as that chunk's kernel is done while the next
+ * chunk computes.  Destination-side tables of gsddmm / gat calls are read at
+ * row row_base + r, row_base = s(q) * R (gsp_partition_chunk_info).
+ * nchunks = 1 is exactly gsp_graph_partition.  Compute semantics as above.
+ * Errors as gsp_graph_partition; ARG also for chunk outside [0, nchunks). */
+gsp_status gsp_graph_partition_chunked(const gsp_graph *g, int nparts, int nchunks, int part, int chunk,
+                                       int device, uint32_t flags, gsp_graph **out);
+
+/* Chunk geometry of a partition (any output may be NULL): nchunks, chunk, and
+ * row_base = the padded row of local row 0.  Full graph: 1, 0, 0. */
+gsp_status gsp_partition_chunk_info(const gsp_graph *g, int *nchunks, int *chunk, int64_t *row_base);
 
 /* Partition geometry (any output may be NULL): nparts, part, global row range
  * [row_begin, row_end), padded rows R, ncols = nparts*R, reverse = 1 for a

@@ -39,8 +39,11 @@ struct DeviceGuard {
     }
 };
 
+// kinds of device bytes (gsp_graph::bytes_by, gsp_graph_memory)
+enum { kTopo = 0, kEid = 1, kEscale = 2, kVertex = 3 };
+
 template <class T>
-gsp_status dev_upload(gsp_graph *g, const T *h, size_t n, const T **out) {
+gsp_status dev_upload(gsp_graph *g, const T *h, size_t n, const T **out, int kind) {
     *out = nullptr;
     if (n == 0) return GSP_OK;
     void *p = nullptr;
@@ -51,13 +54,14 @@ gsp_status dev_upload(gsp_graph *g, const T *h, size_t n, const T **out) {
     }
     g->dev_allocs.push_back(p);
     g->device_bytes += (int64_t)(n * sizeof(T));
+    g->bytes_by[kind] += (int64_t)(n * sizeof(T));
     e = cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy H2D");
     *out = static_cast<const T *>(p);
     return GSP_OK;
 }
 
-gsp_status dev_alloc_f32(gsp_graph *g, size_t n, float **out) {
+gsp_status dev_alloc_f32(gsp_graph *g, size_t n, float **out, int kind) {
     *out = nullptr;
     if (n == 0) return GSP_OK;
     void *p = nullptr;
@@ -68,6 +72,7 @@ gsp_status dev_alloc_f32(gsp_graph *g, size_t n, float **out) {
     }
     g->dev_allocs.push_back(p);
     g->device_bytes += (int64_t)(n * sizeof(float));
+    g->bytes_by[kind] += (int64_t)(n * sizeof(float));
     *out = static_cast<float *>(p);
     return GSP_OK;
 }
@@ -85,11 +90,11 @@ gsp_status make_scales(gsp_graph *g, const std::vector<int64_t> &deg, const floa
     *inv = *rsq = nullptr;
     if (deg.empty()) return GSP_OK;
     const int64_t *d_deg = nullptr;
-    gsp_status st = dev_upload(g, deg.data(), deg.size(), &d_deg);
+    gsp_status st = dev_upload(g, deg.data(), deg.size(), &d_deg, kVertex);
     if (st != GSP_OK) return st;
     float *pi = nullptr, *pr = nullptr;
-    if ((st = dev_alloc_f32(g, deg.size(), &pi)) != GSP_OK) return st;
-    if ((st = dev_alloc_f32(g, deg.size(), &pr)) != GSP_OK) return st;
+    if ((st = dev_alloc_f32(g, deg.size(), &pi, kVertex)) != GSP_OK) return st;
+    if ((st = dev_alloc_f32(g, deg.size(), &pr, kVertex)) != GSP_OK) return st;
     cudaError_t e = gsp::launch_degree_scales(d_deg, (int64_t)deg.size(), pi, pr, 0);
     if (e != cudaSuccess) return cuda_fail(e, "degree_scales launch");
     *inv = pi;
@@ -121,10 +126,10 @@ gsp_status upload_structure(gsp_graph *g, gsp::DevStructure &S, int64_t nrows, i
         S.off = share_topology->off;
         S.col = share_topology->col;
     } else {
-        if ((st = dev_upload(g, off.data(), off.size(), &S.off)) != GSP_OK) return st;
-        if ((st = dev_upload(g, col.data(), col.size(), &S.col)) != GSP_OK) return st;
+        if ((st = dev_upload(g, off.data(), off.size(), &S.off, kTopo)) != GSP_OK) return st;
+        if ((st = dev_upload(g, col.data(), col.size(), &S.col, kTopo)) != GSP_OK) return st;
     }
-    if (eid && (st = dev_upload(g, eid->data(), eid->size(), &S.eid)) != GSP_OK) return st;
+    if (eid && (st = dev_upload(g, eid->data(), eid->size(), &S.eid, kEid)) != GSP_OK) return st;
     auto make_task = [&](const std::vector<int32_t> &order, const int32_t **dst) {
         std::vector<int32_t> task((size_t)nrows * 4);
         for (int64_t i = 0; i < nrows; i++) {
@@ -134,7 +139,7 @@ gsp_status upload_structure(gsp_graph *g, gsp::DevStructure &S, int64_t nrows, i
             task[4 * i + 2] = (int32_t)(uint32_t)((uint64_t)b & 0xffffffffu);
             task[4 * i + 3] = (int32_t)(uint32_t)((uint64_t)b >> 32);
         }
-        return dev_upload(g, task.data(), task.size(), dst);
+        return dev_upload(g, task.data(), task.size(), dst, kVertex);
     };
     std::vector<int32_t> order;
     if (shared_order) {   // same offsets (symmetric topology): same schedule
@@ -144,7 +149,7 @@ gsp_status upload_structure(gsp_graph *g, gsp::DevStructure &S, int64_t nrows, i
         if (eid) gsp::degree_order(off.data(), nrows, heavy_threshold(), order, S.n_heavy);
     } else {
         gsp::degree_order(off.data(), nrows, heavy_threshold(), order, S.n_heavy);
-        if ((st = dev_upload(g, order.data(), order.size(), &S.order)) != GSP_OK) return st;
+        if ((st = dev_upload(g, order.data(), order.size(), &S.order, kVertex)) != GSP_OK) return st;
         if ((st = make_task(order, &S.task)) != GSP_OK) return st;
     }
     static const int64_t win = [] {   // GSP_EID_WIN: id window of the locality schedule (0: off)
@@ -173,12 +178,27 @@ std::vector<int64_t> degrees_of(const std::vector<int64_t> &off) {
 }
 
 // ---------------------------------------------------------------- checks
+// Exact overlap test of two strided fp32 regions {data + 4*(i*ld + c) : i < rows, c < cols}.
+// Regions with the same row stride (e.g. disjoint column slices X = B[:, :F], out = B[:, F:]
+// of one buffer) are resolved exactly; otherwise the exact byte extents are compared.
 bool overlaps(const gsp_tensor *a, const gsp_tensor *b) {
     if (!a || !b || !a->data || !b->data) return false;
-    if (a->rows == 0 || b->rows == 0) return false;
-    auto lo_a = reinterpret_cast<uintptr_t>(a->data), lo_b = reinterpret_cast<uintptr_t>(b->data);
-    auto hi_a = lo_a + (uintptr_t)(a->rows * a->ld) * 4, hi_b = lo_b + (uintptr_t)(b->rows * b->ld) * 4;
-    return lo_a < hi_b && lo_b < hi_a;
+    if (a->rows == 0 || b->rows == 0 || a->cols == 0 || b->cols == 0) return false;
+    const int64_t A0 = (int64_t)reinterpret_cast<uintptr_t>(a->data), B0 = (int64_t)reinterpret_cast<uintptr_t>(b->data);
+    const int64_t hi_a = A0 + ((a->rows - 1) * a->ld + a->cols) * 4, hi_b = B0 + ((b->rows - 1) * b->ld + b->cols) * 4;
+    if (!(A0 < hi_b && B0 < hi_a)) return false;               // disjoint extents
+    if (a->ld != b->ld || (B0 - A0) % 4 != 0) return true;      // conservative beyond this point
+    const int64_t L = a->ld, d = (B0 - A0) / 4;
+    // B row j starts at element d + j*L of A's frame: row q + j, column r (floor division)
+    int64_t q = d / L, r = d % L;
+    if (r < 0) { r += L; q -= 1; }
+    auto rows_meet = [&](int64_t shift) {   // some j in [0, b.rows) with A row q + j + shift in [0, a.rows)
+        const int64_t lo = std::max<int64_t>(0, -(q + shift)), hi = std::min<int64_t>(b->rows, a->rows - (q + shift));
+        return lo < hi;
+    };
+    if (r < a->cols && rows_meet(0)) return true;               // B's row segment [r, r+cb) meets A's [0, ca)
+    if (r + b->cols > L && rows_meet(1)) return true;           // ... or spills into A's next row
+    return false;
 }
 
 gsp_status check_tensor(const gsp_graph *g, const gsp_tensor *t, const char *name, int64_t rows, int64_t cols) {
@@ -279,11 +299,14 @@ static gsp_status upload_full(gsp_graph *g) {
     g->fwd.row_scale[GSP_NORM_BOTH] = rsq_in;
     g->fwd.col_scale[GSP_NORM_BOTH] = rsq_out;
     if (h.has_rev) {
+        // GSP_BUILD_NO_EDGE_IDS: the GCN-lean format keeps no explicit edge ids on
+        // the device; a symmetric graph then holds ONE topology (|V|+|E| words) for both directions
+        const std::vector<int32_t> *rev_eid = g->edge_ids ? &h.rev_eid : nullptr;
         if (h.symmetric)
-            st = upload_structure(g, g->rev, h.V, h.V, h.rev_off, h.rev_col, &h.rev_eid, g->fwd.order,
+            st = upload_structure(g, g->rev, h.V, h.V, h.rev_off, h.rev_col, rev_eid, g->fwd.order,
                                   g->fwd.n_heavy, &g->fwd);
         else
-            st = upload_structure(g, g->rev, h.V, h.V, h.rev_off, h.rev_col, &h.rev_eid, nullptr, 0, nullptr);
+            st = upload_structure(g, g->rev, h.V, h.V, h.rev_off, h.rev_col, rev_eid, nullptr, 0, nullptr);
         if (st != GSP_OK) return st;
         g->rev.row_scale[GSP_NORM_BOTH] = rsq_out;
         g->rev.col_scale[GSP_NORM_RIGHT] = inv_in;
@@ -291,7 +314,7 @@ static gsp_status upload_full(gsp_graph *g) {
     }
     if (g->edge_scales) {
         float *es = nullptr;
-        if ((st = dev_alloc_f32(g, (size_t)h.E, &es)) != GSP_OK) return st;
+        if ((st = dev_alloc_f32(g, (size_t)h.E, &es, kEscale)) != GSP_OK) return st;
         cudaError_t e0 = gsp::launch_gather_scale(g->fwd.col, h.E, rsq_out, es, 0);
         if (e0 != cudaSuccess) return cuda_fail(e0, "edge scales");
         g->fwd.edge_scale[GSP_NORM_BOTH] = es;
@@ -300,7 +323,7 @@ static gsp_status upload_full(gsp_graph *g) {
                 g->rev.edge_scale[GSP_NORM_BOTH] = es;   // d_in == d_out: the same values
             } else {
                 float *er = nullptr;
-                if ((st = dev_alloc_f32(g, (size_t)h.E, &er)) != GSP_OK) return st;
+                if ((st = dev_alloc_f32(g, (size_t)h.E, &er, kEscale)) != GSP_OK) return st;
                 e0 = gsp::launch_gather_scale(g->rev.col, h.E, rsq_in, er, 0);
                 if (e0 != cudaSuccess) return cuda_fail(e0, "edge scales");
                 g->rev.edge_scale[GSP_NORM_BOTH] = er;
@@ -336,7 +359,7 @@ gsp_status gsp_graph_create(int64_t V, int64_t E, const int64_t *src, const int6
     if (E > 0 && (!src || !dst)) return fail(GSP_ERR_NULL, "src/dst is NULL");
     if (V < 0 || E < 0) return fail(GSP_ERR_ARG, "V and E must be >= 0");
     if (flags & ~(uint32_t)(GSP_BUILD_REVERSE | GSP_BUILD_SHARE_SYMMETRIC | GSP_BUILD_EDGE_SCALES |
-                            GSP_BUILD_L2_PERSIST))
+                            GSP_BUILD_L2_PERSIST | GSP_BUILD_NO_EDGE_IDS))
         return fail(GSP_ERR_ARG, "unknown flags");
     if (V >= (int64_t(1) << 31) || E >= (int64_t(1) << 31))
         return fail(GSP_ERR_OVERFLOW, "V and E must be < 2^31 (int32 column and edge ids)");
@@ -366,6 +389,7 @@ gsp_status gsp_graph_create(int64_t V, int64_t E, const int64_t *src, const int6
     g->symmetric = g->host.symmetric;
     g->device = device;
     g->edge_scales = (flags & GSP_BUILD_EDGE_SCALES) != 0;
+    g->edge_ids = (flags & GSP_BUILD_NO_EDGE_IDS) == 0;
     if (device >= 0 && (flags & GSP_BUILD_L2_PERSIST)) raise_l2_setaside(device);
     if (device >= 0) {
         st = upload_full(g);
@@ -419,7 +443,10 @@ gsp_status gsp_gspmm(const gsp_graph *g, const gsp_tensor *X, int norm, gsp_tens
     if ((st = check_compute_graph(g)) != GSP_OK) return st;
     if (norm < GSP_NORM_NONE || norm > GSP_NORM_BOTH) return fail(GSP_ERR_ARG, "norm must be 0, 1 or 2");
     if (reverse != 0 && reverse != 1) return fail(GSP_ERR_ARG, "reverse must be 0 or 1");
-    const gsp::DevStructure &S = reverse ? g->rev : g->fwd;
+    // reverse = 1 on a fwd partition of a directed graph: per-source partials over the
+    // partition's own edges (lrev, [ncols, F]); one reduce-scatter completes them (gsp.h)
+    const bool partials = reverse && !g->rev.present && g->is_partition && g->lrev.present;
+    const gsp::DevStructure &S = reverse ? (partials ? g->lrev : g->rev) : g->fwd;
     if (!S.present)
         return reverse ? fail(GSP_ERR_NO_REVERSE, "graph has no rev structure (GSP_BUILD_REVERSE)")
                        : fail(GSP_ERR_ARG, "this partition only serves reverse = 1");
@@ -781,12 +808,18 @@ gsp_status gsp_partition_bounds(const gsp_graph *g, int nparts, int reverse, int
     return GSP_OK;
 }
 
-gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int device, uint32_t flags,
-                               gsp_graph **out) {
+// Partition (part, chunk) of a full graph: sub-block q = part*nchunks + chunk of the
+// nparts*nchunks edge-balanced C8 blocks, placed at padded slot chunk*nparts + part
+// (chunk-major), so that for every chunk the nparts ranks' [R, F] outputs are one
+// contiguous [nparts*R, F] range of the padded table (one all-gather per chunk).
+static gsp_status partition_impl(const gsp_graph *g, int nparts, int nchunks, int part, int chunk, int device,
+                                 uint32_t flags, gsp_graph **out) {
     if (!g || !out) return fail(GSP_ERR_NULL, "graph/out is NULL");
     *out = nullptr;
     if (g->is_partition) return fail(GSP_ERR_ARG, "graph is already a partition");
     if (nparts < 1 || part < 0 || part >= nparts) return fail(GSP_ERR_ARG, "need 0 <= part < nparts");
+    if (nchunks < 1 || chunk < 0 || chunk >= nchunks) return fail(GSP_ERR_ARG, "need 0 <= chunk < nchunks");
+    if ((int64_t)nparts * nchunks >= (int64_t(1) << 31)) return fail(GSP_ERR_ARG, "nparts * nchunks too large");
     if (flags & ~(uint32_t)GSP_PART_REVERSE) return fail(GSP_ERR_ARG, "unknown flags");
     if (device < -1) return fail(GSP_ERR_ARG, "device must be >= -1");
     const bool prev = (flags & GSP_PART_REVERSE) != 0;
@@ -802,19 +835,23 @@ gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int dev
     const std::vector<int64_t> &off = prev ? h.rev_off : h.fwd_off;
     const std::vector<int32_t> &col = prev ? h.rev_col : h.fwd_col;
     const int64_t V = h.V;
-    std::vector<int64_t> b((size_t)nparts + 1);
-    bounds_of(off, V, nparts, b.data());
+    const int Q = nparts * nchunks;
+    std::vector<int64_t> b((size_t)Q + 1);
+    bounds_of(off, V, Q, b.data());
     int64_t R = 0;
-    for (int p = 0; p < nparts; p++) R = std::max<int64_t>(R, b[p + 1] - b[p]);
-    if ((__int128)nparts * R >= ((__int128)1 << 31)) return fail(GSP_ERR_OVERFLOW, "padded column space >= 2^31");
+    for (int q = 0; q < Q; q++) R = std::max<int64_t>(R, b[q + 1] - b[q]);
+    if ((__int128)Q * R >= ((__int128)1 << 31)) return fail(GSP_ERR_OVERFLOW, "padded column space >= 2^31");
     gsp_graph *pg = new (std::nothrow) gsp_graph();
     if (!pg) return fail(GSP_ERR_OOM, "host allocation failed");
     try {
-        const int64_t rb = b[part], re = b[part + 1], nloc = re - rb, base = off[rb];
+        const int q0 = part * nchunks + chunk;
+        auto slot = [&](int q) { return (int64_t)(q % nchunks) * nparts + q / nchunks; };
+        const int64_t rb = b[q0], re = b[q0 + 1], nloc = re - rb, base = off[rb], row_base = slot(q0) * R;
         std::vector<int32_t> pmap((size_t)V);
-        for (int p = 0; p < nparts; p++)
-            for (int64_t v = b[p]; v < b[p + 1]; v++) pmap[v] = p;
-        auto padded = [&](int64_t v) { return (int64_t)pmap[v] * R + (v - b[pmap[v]]); };
+        for (int q = 0; q < Q; q++)
+            for (int64_t v = b[q]; v < b[q + 1]; v++) pmap[v] = q;
+        auto padded = [&](int64_t v) { return slot(pmap[v]) * R + (v - b[pmap[v]]); };
+        const int64_t NC = (int64_t)Q * R;
         gsp::HostGraph &lh = pg->host;
         lh.V = R;
         lh.E = off[re] - base;
@@ -824,7 +861,6 @@ gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int dev
         for (int64_t j = 0; j < lh.E; j++) lh.fwd_col[j] = (int32_t)padded(col[base + j]);
         if (!prev) {
             // local rev: this partition's edges grouped by padded source, stable in local edge id
-            const int64_t NC = (int64_t)nparts * R;
             lh.rev_off.assign((size_t)NC + 1, 0);
             lh.rev_col.resize((size_t)lh.E);
             lh.rev_eid.resize((size_t)lh.E);
@@ -834,7 +870,7 @@ gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int dev
             for (int64_t r = 0; r < nloc; r++)
                 for (int64_t j = lh.fwd_off[r]; j < lh.fwd_off[r + 1]; j++) {
                     const int64_t k = pos[lh.fwd_col[j]]++;
-                    lh.rev_col[k] = (int32_t)((int64_t)part * R + r);
+                    lh.rev_col[k] = (int32_t)(row_base + r);
                     lh.rev_eid[k] = (int32_t)j;
                 }
             lh.has_rev = true;
@@ -842,17 +878,20 @@ gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int dev
         pg->is_partition = true;
         pg->nparts = nparts;
         pg->part = part;
+        pg->nchunks = nchunks;
+        pg->chunk = chunk;
         pg->part_reverse = prev ? 1 : 0;
         pg->row_begin = rb;
         pg->row_end = re;
         pg->R = R;
-        pg->row_base = (int64_t)part * R;
+        pg->row_base = row_base;
         pg->nrows = R;
-        pg->ncols = (int64_t)nparts * R;
+        pg->ncols = NC;
         pg->V_global = V;
         pg->E = lh.E;
         pg->symmetric = h.symmetric;
         pg->device = device;
+        pg->edge_ids = g->edge_ids;
         if (device >= 0) {
             DeviceGuard dg(device);
             gsp_status st;
@@ -864,7 +903,7 @@ gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int dev
                 for (int32_t u : h.fwd_col) dout[u]++;
             }
             std::vector<int64_t> loc_in((size_t)R, 1), loc_out((size_t)R, 1);
-            std::vector<int64_t> pad_in((size_t)nparts * R, 1), pad_out((size_t)nparts * R, 1);
+            std::vector<int64_t> pad_in((size_t)NC, 1), pad_out((size_t)NC, 1);
             for (int64_t r = 0; r < nloc; r++) { loc_in[r] = din[rb + r]; loc_out[r] = dout[rb + r]; }
             for (int64_t v = 0; v < V; v++) { pad_in[padded(v)] = din[v]; pad_out[padded(v)] = dout[v]; }
             const float *li_inv, *li_rsq, *lo_inv, *lo_rsq, *pi_inv, *pi_rsq, *po_inv, *po_rsq;
@@ -880,8 +919,7 @@ gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int dev
             (void)lo_inv; (void)po_inv;
             gsp::DevStructure *fw = prev ? nullptr : &pg->fwd;
             if (fw) {
-                st = upload_structure(pg, *fw, R, (int64_t)nparts * R, lh.fwd_off, lh.fwd_col, nullptr, nullptr, 0,
-                                      nullptr);
+                st = upload_structure(pg, *fw, R, NC, lh.fwd_off, lh.fwd_col, nullptr, nullptr, 0, nullptr);
                 if (st == GSP_OK) {
                     fw->row_scale[GSP_NORM_RIGHT] = li_inv;
                     fw->row_scale[GSP_NORM_BOTH] = li_rsq;
@@ -891,26 +929,36 @@ gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int dev
             // rev view: a GSP_PART_REVERSE partition, or the shared topology of a symmetric graph
             if (st == GSP_OK && (prev || h.symmetric)) {
                 if (prev)
-                    st = upload_structure(pg, pg->rev, R, (int64_t)nparts * R, lh.fwd_off, lh.fwd_col, nullptr,
-                                          nullptr, 0, nullptr);
+                    st = upload_structure(pg, pg->rev, R, NC, lh.fwd_off, lh.fwd_col, nullptr, nullptr, 0, nullptr);
                 else
-                    st = upload_structure(pg, pg->rev, R, (int64_t)nparts * R, lh.fwd_off, lh.fwd_col, nullptr,
-                                          pg->fwd.order, pg->fwd.n_heavy, &pg->fwd);
+                    st = upload_structure(pg, pg->rev, R, NC, lh.fwd_off, lh.fwd_col, nullptr, pg->fwd.order,
+                                          pg->fwd.n_heavy, &pg->fwd);
                 if (st == GSP_OK) {
-                    pg->rev.eid = nullptr;  // weighted reverse on partitions: not provided
+                    pg->rev.eid = nullptr;  // weighted reverse on partitions: the lrev partials (below)
                     pg->rev.row_scale[GSP_NORM_BOTH] = lo_rsq;
                     pg->rev.col_scale[GSP_NORM_RIGHT] = pi_inv;
                     pg->rev.col_scale[GSP_NORM_BOTH] = pi_rsq;
                 }
             }
-            if (st == GSP_OK && !prev) {
-                st = upload_structure(pg, pg->lrev, (int64_t)nparts * R, (int64_t)nparts * R, lh.rev_off, lh.rev_col,
-                                      &lh.rev_eid, nullptr, 0, nullptr);
+            // local rev (fwd partitions): per-source partials of the weighted reverse
+            // (explicit local edge ids) and, on a directed graph, of the scaled reverse
+            // gSpMMv (rows = padded sources: s_src = d_out^-1/2, columns = this part's
+            // destinations: s_dst = 1/d_in or d_in^-1/2).  GSP_BUILD_NO_EDGE_IDS keeps
+            // only what the scaled reverse needs: nothing on a symmetric graph (its
+            // reverse is the shared topology above), the topology on a directed one.
+            if (st == GSP_OK && !prev && (g->edge_ids || !h.symmetric)) {
+                st = upload_structure(pg, pg->lrev, NC, NC, lh.rev_off, lh.rev_col, g->edge_ids ? &lh.rev_eid : nullptr,
+                                      nullptr, 0, nullptr);
+                if (st == GSP_OK) {
+                    pg->lrev.row_scale[GSP_NORM_BOTH] = po_rsq;
+                    pg->lrev.col_scale[GSP_NORM_RIGHT] = pi_inv;
+                    pg->lrev.col_scale[GSP_NORM_BOTH] = pi_rsq;
+                }
             }
             if (st == GSP_OK && g->edge_scales && lh.E > 0) {
                 pg->edge_scales = true;
                 float *es = nullptr;
-                if ((st = dev_alloc_f32(pg, (size_t)lh.E, &es)) == GSP_OK) {
+                if ((st = dev_alloc_f32(pg, (size_t)lh.E, &es, kEscale)) == GSP_OK) {
                     // fwd partition: column side = sources (d_out); reverse partition: destinations (d_in)
                     const gsp::DevStructure &own = prev ? pg->rev : pg->fwd;
                     cudaError_t e0 = gsp::launch_gather_scale(own.col, lh.E, prev ? pi_rsq : po_rsq, es, 0);
@@ -939,6 +987,34 @@ gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int dev
         return fail(GSP_ERR_OOM, "host allocation failed in partition");
     }
     *out = pg;
+    return GSP_OK;
+}
+
+gsp_status gsp_graph_partition(const gsp_graph *g, int nparts, int part, int device, uint32_t flags,
+                               gsp_graph **out) {
+    return partition_impl(g, nparts, 1, part, 0, device, flags, out);
+}
+
+gsp_status gsp_graph_partition_chunked(const gsp_graph *g, int nparts, int nchunks, int part, int chunk, int device,
+                                       uint32_t flags, gsp_graph **out) {
+    return partition_impl(g, nparts, nchunks, part, chunk, device, flags, out);
+}
+
+gsp_status gsp_partition_chunk_info(const gsp_graph *g, int *nchunks, int *chunk, int64_t *row_base) {
+    if (!g) return fail(GSP_ERR_NULL, "graph is NULL");
+    if (nchunks) *nchunks = g->nchunks;
+    if (chunk) *chunk = g->chunk;
+    if (row_base) *row_base = g->row_base;
+    return GSP_OK;
+}
+
+gsp_status gsp_graph_memory(const gsp_graph *g, int64_t *topology, int64_t *edge_ids, int64_t *edge_scales,
+                            int64_t *vertex_arrays) {
+    if (!g) return fail(GSP_ERR_NULL, "graph is NULL");
+    if (topology) *topology = g->bytes_by[kTopo];
+    if (edge_ids) *edge_ids = g->bytes_by[kEid];
+    if (edge_scales) *edge_scales = g->bytes_by[kEscale];
+    if (vertex_arrays) *vertex_arrays = g->bytes_by[kVertex];
     return GSP_OK;
 }
 

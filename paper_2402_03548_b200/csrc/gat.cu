@@ -1,4 +1,6 @@
 // Fused GAT forward (NEXT-2).
+#include <atomic>
+
 #include "common.cuh"
 
 namespace gsp {
@@ -409,19 +411,43 @@ static int64_t gat_score_bytes() {
     return v;
 }
 
+// Opt a kernel in to > 48 KB of dynamic shared memory once per device.  The
+// per-(kernel, device) flags are atomics: concurrent first calls on different
+// threads / streams (gsp.h: compute calls are thread-safe) at worst both set the
+// (idempotent) attribute; no data race.
+using AttrFlags = std::atomic<int>[64];
+template <class K>
+cudaError_t opt_in_smem(K kernel, size_t dyn, AttrFlags &flags) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 64 && flags[dev].load(std::memory_order_acquire) >= (int)dyn) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    if (dev < 64) {
+        int cur = flags[dev].load(std::memory_order_relaxed);
+        while (cur < (int)dyn && !flags[dev].compare_exchange_weak(cur, (int)dyn, std::memory_order_release)) {
+        }
+    }
+    return cudaSuccess;
+}
+template <int HH, bool SAME>
+AttrFlags &gat_fused_attr() {
+    static AttrFlags f{};
+    return f;
+}
+template <int HH>
+AttrFlags &gat_bwd_attr() {
+    static AttrFlags f{};
+    return f;
+}
+
 template <int HH, bool SAME>
 cudaError_t launch_gat_h(GatArgs a, dim3 grid, cudaStream_t s) {
     a.sc_cap = (gat_score_bytes() / (4 * HH)) & ~int64_t(31);   // whole 32-edge tiles
     const size_t dyn = (size_t)(kWarps * a.sc_cap * HH * 4);
-    static bool attr[64] = {};   // opt in to > 48 KB of dynamic shared memory once per device
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
+    cudaError_t e = opt_in_smem(gat_fused_kernel<HH, SAME>, dyn, gat_fused_attr<HH, SAME>());
     if (e != cudaSuccess) return e;
-    if (dev >= 64 || !attr[dev]) {
-        e = cudaFuncSetAttribute(gat_fused_kernel<HH, SAME>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        if (e != cudaSuccess) return e;
-        if (dev < 64) attr[dev] = true;
-    }
     gat_fused_kernel<HH, SAME><<<grid, kThreads, dyn, s>>>(a);
     return cudaGetLastError();
 }
@@ -446,15 +472,8 @@ template <int HH>
 cudaError_t launch_gat_bwd_h(GatArgs a, dim3 grid, cudaStream_t s) {
     a.sc_cap = (gat_score_bytes() / (4 * HH)) & ~int64_t(31);
     const size_t dyn = (size_t)(kWarps * a.sc_cap * HH * 4);
-    static bool attr[64] = {};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
+    cudaError_t e = opt_in_smem(gat_bwd_kernel<HH>, dyn, gat_bwd_attr<HH>());
     if (e != cudaSuccess) return e;
-    if (dev >= 64 || !attr[dev]) {
-        e = cudaFuncSetAttribute(gat_bwd_kernel<HH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        if (e != cudaSuccess) return e;
-        if (dev < 64) attr[dev] = true;
-    }
     gat_bwd_kernel<HH><<<grid, kThreads, dyn, s>>>(a);
     return cudaGetLastError();
 }

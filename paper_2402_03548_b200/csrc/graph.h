@@ -72,9 +72,10 @@ struct gsp_graph {
     int64_t nrows = 0, ncols = 0, E = 0;       // nrows = V (full) or R (partition)
     int64_t V_global = 0;
     bool symmetric = false;
-    // partition geometry
+    // partition geometry (chunked: sub-block q = part*nchunks + chunk of nparts*nchunks
+    // C8 blocks sits at padded slot chunk*nparts + part; row_base = slot*R)
     bool is_partition = false;
-    int nparts = 1, part = 0, part_reverse = 0;
+    int nparts = 1, part = 0, part_reverse = 0, nchunks = 1, chunk = 0;
     int64_t row_begin = 0, row_end = 0, R = 0, row_base = 0;
     // host mirror (full graphs: HostGraph; fwd partitions: local fwd + local rev (lrev))
     gsp::HostGraph host;
@@ -84,5 +85,10 @@ struct gsp_graph {
     gsp::DevStructure fwd, rev, lrev;
     std::vector<void *> dev_allocs;
     int64_t device_bytes = 0;
+    // device bytes by kind (gsp_graph_memory): topology (offsets + column ids, the
+    // paper's |V|+|E| words per stored structure), explicit edge ids,
+    // per-edge scales, vertex arrays (degree scales, row schedules)
+    int64_t bytes_by[4] = {0, 0, 0, 0};
     bool edge_scales = false;
+    bool edge_ids = true;      // false: GSP_BUILD_NO_EDGE_IDS (no rev_eid / lrev on the device)
 };

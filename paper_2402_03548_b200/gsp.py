@@ -21,7 +21,7 @@ NORM_NONE, NORM_RIGHT, NORM_BOTH = 0, 1, 2
 REDUCE_SUM, REDUCE_MIN, REDUCE_MAX = 0, 1, 2
 OP_ADD, OP_SUB, OP_MUL, OP_DIV = 0, 1, 2, 3
 SIDE_DST, SIDE_SRC = 0, 1
-BUILD_REVERSE, BUILD_SHARE_SYMMETRIC, BUILD_EDGE_SCALES, BUILD_L2_PERSIST = 1, 2, 4, 8
+BUILD_REVERSE, BUILD_SHARE_SYMMETRIC, BUILD_EDGE_SCALES, BUILD_L2_PERSIST, BUILD_NO_EDGE_IDS = 1, 2, 4, 8, 16
 PART_REVERSE = 1
 
 STATUS = {0: "GSP_OK", 1: "GSP_ERR_NULL", 2: "GSP_ERR_ARG", 3: "GSP_ERR_VERTEX_RANGE", 4: "GSP_ERR_SHAPE",
@@ -31,6 +31,7 @@ STATUS = {0: "GSP_OK", 1: "GSP_ERR_NULL", 2: "GSP_ERR_ARG", 3: "GSP_ERR_VERTEX_R
 SYMBOLS = ["gsp_graph_create", "gsp_graph_destroy", "gsp_graph_info", "gsp_graph_export", "gsp_gspmm",
            "gsp_gspmm_weighted", "gsp_gsddmm", "gsp_edge_softmax", "gsp_edge_softmax_backward",
            "gsp_gat_forward", "gsp_gat_backward_scores", "gsp_gspmm_reduce", "gsp_gspmm_e", "gsp_gsddmm_ve", "gsp_partition_bounds", "gsp_graph_partition",
+           "gsp_graph_partition_chunked", "gsp_partition_chunk_info", "gsp_graph_memory",
            "gsp_partition_info", "gsp_status_string", "gsp_last_error_detail", "gsp_version"]
 
 
@@ -71,6 +72,9 @@ def _load():
         "gsp_gsddmm_ve": ([p, T, T, ci, ci, T, p], ci),
         "gsp_partition_bounds": ([p, ci, ci, p], ci),
         "gsp_graph_partition": ([p, ci, ci, ci, u32, P(p)], ci),
+        "gsp_graph_partition_chunked": ([p, ci, ci, ci, ci, ci, u32, P(p)], ci),
+        "gsp_partition_chunk_info": ([p, P(ci), P(ci), P(i64)], ci),
+        "gsp_graph_memory": ([p, P(i64), P(i64), P(i64), P(i64)], ci),
         "gsp_partition_info": ([p, P(ci), P(ci), P(i64), P(i64), P(i64), P(i64), P(ci)], ci),
         "gsp_status_string": ([ci], ctypes.c_char_p),
         "gsp_last_error_detail": ([], ctypes.c_char_p),
@@ -100,8 +104,16 @@ def _desc(t):
         raise ValueError("gsp tensors are 2-D [rows, cols]")
     if t.shape[1] > 1 and t.stride(1) != 1:
         raise ValueError("gsp tensors need unit column stride")
-    ld = t.stride(0) if t.shape[0] > 1 else max(t.shape[1], t.stride(0))
-    return gsp_tensor(t.data_ptr(), t.shape[0], t.shape[1], max(ld, t.shape[1]))
+    if t.shape[0] > 1:
+        # the row stride goes through unchanged: a broadcast / overlapping-row view
+        # (stride(0) < cols, e.g. expand()) is rejected here and by the library's SHAPE check
+        if t.stride(0) < t.shape[1]:
+            raise ValueError(f"gsp tensors need row stride >= cols (got stride {t.stride(0)} for "
+                             f"{t.shape[1]} columns: broadcast or overlapping rows)")
+        ld = t.stride(0)
+    else:   # a single row: any stride is valid, report the tightest one
+        ld = max(t.shape[1], t.stride(0))
+    return gsp_tensor(t.data_ptr(), t.shape[0], t.shape[1], ld)
 
 
 def _stream(stream, device):
@@ -116,7 +128,7 @@ class Graph:
     """Kernel-graph handle (GraphPy's `g`) owning a libgsp graph."""
 
     def __init__(self, V=None, src=None, dst=None, *, reverse=True, share_symmetric=True, edge_scales=True,
-                 l2_persist=False, device=0, _handle=None):
+                 l2_persist=False, edge_ids=True, device=0, _handle=None):
         self._h = ctypes.c_void_p()
         if _handle is not None:
             self._h = _handle
@@ -126,7 +138,8 @@ class Graph:
             if src.shape != dst.shape or src.ndim != 1:
                 raise ValueError("src and dst must be 1-D arrays of equal length")
             flags = (BUILD_REVERSE if reverse else 0) | (BUILD_SHARE_SYMMETRIC if share_symmetric else 0) | \
-                (BUILD_EDGE_SCALES if edge_scales else 0) | (BUILD_L2_PERSIST if l2_persist else 0)
+                (BUILD_EDGE_SCALES if edge_scales else 0) | (BUILD_L2_PERSIST if l2_persist else 0) | \
+                (0 if edge_ids else BUILD_NO_EDGE_IDS)
             _check(lib.gsp_graph_create(int(V), src.shape[0], src.ctypes.data, dst.ctypes.data, flags,
                                         int(device), ctypes.byref(self._h)))
         V_, E_, b_, s_ = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
@@ -134,6 +147,10 @@ class Graph:
         self.V, self.E, self.device_bytes, self.symmetric = V_.value, E_.value, b_.value, bool(s_.value)
         info = self.partition_info()
         self.nparts, self.part, self.row_begin, self.row_end, self.R, self.ncols, self.part_reverse = info
+        nc, ch, rb = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+        _check(lib.gsp_partition_chunk_info(self._h, ctypes.byref(nc), ctypes.byref(ch), ctypes.byref(rb)))
+        self.nchunks, self.chunk, self.row_base = nc.value, ch.value, rb.value
+        self.is_partition = _handle is not None   # handles come from partition()
         self.device = device
 
     def close(self):
@@ -177,20 +194,34 @@ class Graph:
         _check(lib.gsp_partition_bounds(self._h, int(nparts), int(bool(reverse)), b.ctypes.data))
         return b
 
-    def partition(self, nparts, part, device=0, reverse=False):
+    def partition(self, nparts, part, device=0, reverse=False, nchunks=1, chunk=0):
+        """Partition `part` of `nparts` (gsp_graph_partition); with nchunks > 1 the
+        chunk `chunk` of it in the chunk-major padded layout (gsp_graph_partition_chunked)."""
         h = ctypes.c_void_p()
-        _check(lib.gsp_graph_partition(self._h, int(nparts), int(part), int(device),
-                                       PART_REVERSE if reverse else 0, ctypes.byref(h)))
+        _check(lib.gsp_graph_partition_chunked(self._h, int(nparts), int(nchunks), int(part), int(chunk),
+                                               int(device), PART_REVERSE if reverse else 0, ctypes.byref(h)))
         return Graph(_handle=h, device=device)
+
+    def memory(self):
+        """Device bytes by kind (gsp_graph_memory): topology, edge_ids, edge_scales, vertex_arrays."""
+        a = [ctypes.c_int64() for _ in range(4)]
+        _check(lib.gsp_graph_memory(self._h, *[ctypes.byref(x) for x in a]))
+        return dict(zip(("topology", "edge_ids", "edge_scales", "vertex_arrays"), (x.value for x in a)))
 
     # ------------------------------------------------------------ compute
     def _alloc(self, rows, cols, like):
         import torch
         return torch.empty((rows, cols), dtype=torch.float32, device=like.device)
 
+    def reverse_gives_partials(self):
+        """reverse = 1 gSpMMv on this graph yields per-source partials [ncols, F]
+        (a fwd partition of a directed graph; gsp.h gsp_graph_partition)."""
+        return self.is_partition and not self.part_reverse and not self.symmetric
+
     def gspmm(self, X, norm=NORM_BOTH, out=None, reverse=False, stream=None):
         if out is None:
-            out = self._alloc(self.V, X.shape[1], X)
+            rows = self.ncols if (reverse and self.reverse_gives_partials()) else self.V
+            out = self._alloc(rows, X.shape[1], X)
         dx, do = _desc(X), _desc(out)
         _check(lib.gsp_gspmm(self._h, ctypes.byref(dx), int(norm), ctypes.byref(do), int(bool(reverse)),
                              _stream(stream, X.device)))
