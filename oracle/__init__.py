@@ -76,6 +76,11 @@ def _L():
         lib.oracle_partition_bounds.restype = ci
         lib.oracle_partition_structure.argtypes = [i64, p, p, i64, p, i64, p, p]
         lib.oracle_partition_structure.restype = ci
+        d = ctypes.c_double
+        lib.oracle_gsddmm_add_leaky.argtypes = [i64, p, p, p, p, i64, i64, d, p]
+        lib.oracle_gsddmm_add_leaky.restype = ci
+        lib.oracle_gat_forward_additive.argtypes = [i64, p, p, p, p, i64, p, i64, i64, i64, d, p, p, p, p]
+        lib.oracle_gat_forward_additive.restype = ci
         _lib = lib
     return _lib
 
@@ -217,6 +222,36 @@ class Graph:
         rc = _L().oracle_gat_forward(self.V, _ptr(self.fwd_off), _ptr(self.fwd_col), _ptr(X), X.shape[1], _ptr(Y),
                                      Y.shape[1], F, _ptr(Vt), Vt.shape[1], Fv, H, _ptr(alpha), _ptr(out), _ptr(T),
                                      _ptr(scratch))
+        assert rc == 0, rc
+        return alpha, out, T
+
+    # --- C14, C15 (NEXT-3: additive GAT attention)
+    def gsddmm_add_leaky(self, el, er, slope=0.2):
+        """C14: out[j,h] = leaky_relu(el[u_j,h] + er[v,h], slope) fp64 [E,H]; el/er fp32 [V,H]."""
+        el = _c(el, np.float32)
+        er = _c(er, np.float32)
+        assert el.shape == er.shape
+        H = el.shape[1]
+        out = np.empty((self.E, H), np.float64)
+        rc = _L().oracle_gsddmm_add_leaky(self.V, _ptr(self.fwd_off), _ptr(self.fwd_col), _ptr(el), _ptr(er), H, H,
+                                          float(slope), _ptr(out))
+        assert rc == 0, rc
+        return out
+
+    def gat_forward_additive(self, el, er, Vt, slope=0.2):
+        """C15: (alpha [E,H], out [V,Fv], T_out) in fp64: softmax(C14(el, er)) then weighted sum of Vt."""
+        el = _c(el, np.float32)
+        er = _c(er, np.float32)
+        Vt = _c(Vt, np.float32)
+        H, Fv = el.shape[1], Vt.shape[1]
+        alpha = np.empty((self.E, H), np.float64)
+        out = np.empty((self.V, Fv), np.float64)
+        T = np.empty((self.V, Fv), np.float64)
+        maxdeg = int(np.max(np.diff(self.fwd_off))) if self.V else 0
+        scratch = np.empty(max(maxdeg, 1), np.float64)
+        rc = _L().oracle_gat_forward_additive(self.V, _ptr(self.fwd_off), _ptr(self.fwd_col), _ptr(el), _ptr(er), H,
+                                              _ptr(Vt), Fv, Fv, H, float(slope), _ptr(alpha), _ptr(out), _ptr(T),
+                                              _ptr(scratch))
         assert rc == 0, rc
         return alpha, out, T
 

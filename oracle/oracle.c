@@ -526,3 +526,63 @@ int oracle_partition_structure(int64_t V, const int64_t *off, const int32_t *col
     }
     return 0;
 }
+
+/* ---------------------------------------------------------- C14, C15 --- */
+/* Additive (GAT) attention scores: Table 1's gSDDMM family with an add instead
+ * of a dot product ("gSDDMMve ... vertex-level and
+ * edge-level tensors ... to arrive at the resultant edge-level tensor", here
+ * the u_add_v form of both endpoints' per-head vertex scalars), followed by the
+ * leaky ReLU of the standard GAT attention ("edge logit[j,h] =
+ * leaky_relu(<a_src, z[.]> + <a_dst, z[.]>, slope)", slope 0.2 at S:411):
+ *   C14: out[j,h] = lrelu(el[u_j, h] + er[v, h]),  lrelu(x) = x if x > 0 else slope * x
+ * for slot j of fwd row v with column (source) u_j.  el [V, lde] is the source
+ * side, er [V, lde] the destination side (H columns used), both fp32; the sum
+ * and the product are taken in fp64. */
+int oracle_gsddmm_add_leaky(int64_t V, const int64_t *fwd_off, const int32_t *fwd_col, const float *el,
+                            const float *er, int64_t lde, int64_t H, double slope, double *out) {
+    for (int64_t v = 0; v < V; v++)
+        for (int64_t j = fwd_off[v]; j < fwd_off[v + 1]; j++) {
+            int64_t u = fwd_col[j];
+            for (int64_t h = 0; h < H; h++) {
+                double x = (double)el[u * lde + h] + (double)er[v * lde + h];
+                out[j * H + h] = x > 0.0 ? x : slope * x;
+            }
+        }
+    return 0;
+}
+
+/* C15: the fused additive GAT forward (NEXT-3 + NEXT-2): alpha = C7(C14(el,
+ * er)) and out[v, h*Fvh+f] = sum_j alpha[j,h] Vt[u_j, h*Fvh+f] (C5), all in
+ * fp64 with no fp32 hand-off between the steps; T_out = sum_j alpha |Vt|. */
+int oracle_gat_forward_additive(int64_t V, const int64_t *fwd_off, const int32_t *fwd_col, const float *el,
+                                const float *er, int64_t lde, const float *Vt, int64_t ldv, int64_t Fv, int64_t H,
+                                double slope, double *alpha, double *out, double *Tout, double *scratch) {
+    if (H <= 0 || Fv % H != 0) return -2;
+    int64_t Fvh = Fv / H;
+    for (int64_t v = 0; v < V; v++) {
+        int64_t b = fwd_off[v], e = fwd_off[v + 1];
+        for (int64_t h = 0; h < H; h++) {
+            double m = -INFINITY;
+            for (int64_t j = b; j < e; j++) {
+                double x = (double)el[(int64_t)fwd_col[j] * lde + h] + (double)er[v * lde + h];
+                double sc = x > 0.0 ? x : slope * x;
+                scratch[j - b] = sc;
+                if (sc > m) m = sc;
+            }
+            double S = 0.0;
+            for (int64_t j = b; j < e; j++) S += exp(scratch[j - b] - m);
+            for (int64_t j = b; j < e; j++) alpha[j * H + h] = exp(scratch[j - b] - m) / S;
+            for (int64_t f = 0; f < Fvh; f++) {
+                double acc = 0.0, tacc = 0.0;
+                for (int64_t j = b; j < e; j++) {
+                    double t = alpha[j * H + h] * (double)Vt[(int64_t)fwd_col[j] * ldv + h * Fvh + f];
+                    acc += t;
+                    tacc += fabs(t);
+                }
+                out[v * Fv + h * Fvh + f] = acc;
+                if (Tout) Tout[v * Fv + h * Fvh + f] = tacc;
+            }
+        }
+    }
+    return 0;
+}

@@ -97,6 +97,13 @@ gsp_status make_scales(gsp_graph *g, const std::vector<int64_t> &deg, const floa
     if ((st = dev_alloc_f32(g, deg.size(), &pr, kVertex)) != GSP_OK) return st;
     cudaError_t e = gsp::launch_degree_scales(d_deg, (int64_t)deg.size(), pi, pr, 0);
     if (e != cudaSuccess) return cuda_fail(e, "degree_scales launch");
+    // the integer degrees are only an input of the scale kernel: release them
+    // (cudaFree waits for the kernel) so the graph keeps O(V) fp32 scales only
+    e = cudaFree(const_cast<int64_t *>(d_deg));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFree");
+    g->dev_allocs.erase(std::find(g->dev_allocs.begin(), g->dev_allocs.end(), (void *)d_deg));
+    g->device_bytes -= (int64_t)(deg.size() * sizeof(int64_t));
+    g->bytes_by[kVertex] -= (int64_t)(deg.size() * sizeof(int64_t));
     *inv = pi;
     *rsq = pr;
     return GSP_OK;

@@ -215,3 +215,92 @@ def test_partition_local_rev_bitexact(gsp, seed):
             assert np.array_equal(ex["rev_eid"], order.astype(np.int32))
             assert np.array_equal(ex["rev_col"], (p * R + rows[order]).astype(np.int32))
             assert np.array_equal(ex["rev_off"], np.concatenate([[0], np.cumsum(np.bincount(lc, minlength=P * R))]))
+
+
+# ------------------------------------------------------- chunked partitions
+def chunked_expected(og, P, C, p, c, reverse=False):
+    """Brute force of the chunk-major layout (include/gsp.h gsp_graph_partition_chunked):
+    blocks = oracle C8 bounds with Q = P*C parts, block q = p*C + c at slot (q % C)*P + q // C."""
+    Q = P * C
+    b = og.partition_bounds(Q, reverse)
+    R = int(np.max(np.diff(b)))
+    off = og.rev_off if reverse else og.fwd_off
+    col = og.rev_col if reverse else og.fwd_col
+    qmap = np.searchsorted(b, np.arange(og.V), side="right") - 1      # block of every vertex
+    slot = (qmap % C) * P + qmap // C
+    padded = slot * R + (np.arange(og.V) - b[qmap])
+    q = p * C + c
+    lo, hi = b[q], b[q + 1]
+    loc_off = off[np.minimum(lo + np.arange(R + 1), hi)] - off[lo]
+    loc_col = padded[col[off[lo]:off[hi]]].astype(np.int32)
+    return loc_off, loc_col, R, b, ((q % C) * P + q // C) * R
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_chunked_partition_structure_bitexact(gsp, seed):
+    rng = np.random.default_rng(700 + seed)
+    V = int(rng.integers(1, 300))
+    E = int(rng.integers(0, 2500))
+    src, dst = datagen.random_multigraph(V, E, seed)
+    G = host_graph(gsp, V, src, dst)
+    og = oracle.Graph(V, src, dst)
+    for P, C in ((1, 3), (2, 2), (2, 3), (3, 4), (4, 1)):
+        for rev in (False, True):
+            # the rows a rank owns are those of the unchunked partition
+            bP = og.partition_bounds(P, rev)
+            assert np.array_equal(G.partition_bounds(P * C, rev)[::C], bP)
+            seen = 0
+            for p in range(P):
+                for c in range(C):
+                    pg = G.partition(P, p, device=-1, reverse=rev, nchunks=C, chunk=c)
+                    lo, lc, R, b, rb = chunked_expected(og, P, C, p, c, rev)
+                    ex = pg.export(rev=False, coo=False)
+                    assert np.array_equal(ex["fwd_off"], lo) and np.array_equal(ex["fwd_col"], lc)
+                    q = p * C + c
+                    assert (pg.nparts, pg.part, pg.nchunks, pg.chunk, pg.row_begin, pg.row_end, pg.R, pg.ncols,
+                            pg.row_base) == (P, p, C, c, b[q], b[q + 1], R, P * C * R, rb)
+                    seen += pg.E
+            assert seen == og.E
+            if C == 1:   # nchunks = 1 is exactly gsp_graph_partition
+                for p in range(P):
+                    a = G.partition(P, p, device=-1, reverse=rev).export(rev=False, coo=False)
+                    lo, lc, R, b = og.partition_structure(P, p, rev)
+                    assert np.array_equal(a["fwd_off"], lo) and np.array_equal(a["fwd_col"], lc)
+
+
+def test_chunked_partition_local_rev(gsp):
+    """Local rev of a chunk: its own edges grouped by padded source, rev_col = row_base + local row."""
+    src, dst = datagen.random_multigraph(120, 900, 3)
+    G = host_graph(gsp, 120, src, dst)
+    og = oracle.Graph(120, src, dst)
+    P, C = 2, 3
+    for p in range(P):
+        for c in range(C):
+            pg = G.partition(P, p, device=-1, nchunks=C, chunk=c)
+            lo, lc, R, b, rb = chunked_expected(og, P, C, p, c)
+            ex = pg.export(rev=True, coo=False)
+            rows = np.repeat(np.arange(R), np.diff(lo))
+            order = np.argsort(lc, kind="stable")
+            assert np.array_equal(ex["rev_eid"], order.astype(np.int32))
+            assert np.array_equal(ex["rev_col"], (rb + rows[order]).astype(np.int32))
+
+
+def test_chunked_partition_errors(gsp, golden):
+    g = golden("d4.json")
+    G = host_graph(gsp, g["V"], g["src"], g["dst"])
+    for P, C, p, c in ((2, 0, 0, 0), (2, 2, 0, 2), (2, 2, 0, -1), (2, 2, 2, 0)):
+        with pytest.raises(gsp.GspError) as ei:
+            G.partition(P, p, device=-1, nchunks=C, chunk=c)
+        assert ei.value.name == "GSP_ERR_ARG"
+
+
+def test_no_edge_ids_flag_host(gsp, golden):
+    """GSP_BUILD_NO_EDGE_IDS changes only the device format: the host structure
+    (export) is the canonical one, and a host-only graph holds no device bytes."""
+    for gf in ("t4.json", "d4.json"):
+        g = golden(gf)
+        G = host_graph(gsp, g["V"], g["src"], g["dst"], edge_ids=False)
+        ex = G.export()
+        assert ex["fwd_col"].tolist() == g["fwd_col"] and ex["rev_eid"].tolist() == g["rev_eid"]
+        assert G.memory() == {"topology": 0, "edge_ids": 0, "edge_scales": 0, "vertex_arrays": 0}
+        assert G.device_bytes == 0

@@ -421,9 +421,9 @@ def _gat_check(gsp, V, src, dst, H, Fh, Fv, same, ld=None, seed=0):
     Y = dev(Yh)
     Vt = Y if same else dev(Vh)
     alpha, out = G.gat_forward(X, Y, Vt, H)
-    # tolerances: alpha 2e-5 absolute, out 2e-5 (T + 1)
+    # north_star bound: alpha 1e-5 (1 + 1) absolute, out 1e-5 (T + 1)
     assert_within(alpha.cpu().numpy(), a_ref, 1.0, f"alpha H{H} Fh{Fh}")
-    assert_within(out.cpu().numpy(), o_ref, T, f"out H{H} Fh{Fh}", scale=2e-5)
+    assert_within(out.cpu().numpy(), o_ref, T, f"out H{H} Fh{Fh}")
 
 
 @pytest.mark.parametrize("H,Fh,Fv,same", [(8, 8, 8, True), (8, 8, 8, False), (2, 8, 8, True), (4, 8, 8, False),
@@ -598,7 +598,7 @@ def test_boundary_degrees_all_ops(gsp):
     a_ref, o_ref, T = og.gat_forward(Zh, Zh, Zh, H)
     alpha, out = G.gat_forward(dev(Zh), dev(Zh), dev(Zh), H)
     assert_within(alpha.cpu().numpy(), a_ref, 1.0, "gat alpha")
-    assert_within(out.cpu().numpy(), o_ref, T, "gat out", scale=2e-5)
+    assert_within(out.cpu().numpy(), o_ref, T, "gat out")
 
 
 def test_cuda_graph_capture_replay(gsp):
@@ -710,3 +710,173 @@ def test_odd_output_stride_keeps_vector_gathers(gsp):
         out = padded(np.full((V, H * Fh), np.nan, np.float32), ldo)
         G.gspmm_weighted(dev(Xh), dev(wh), out=out, reverse=rev)
         assert_within(out.cpu().numpy(), ref, T, f"weighted ldo{ldo} r{rev}")
+
+
+# ------------------------------------------------- chunked partitions (A9)
+def chunk_layout(G, P, C):
+    """(bounds of the P*C blocks, slot of block q, R) of the chunk-major layout."""
+    b = G.partition_bounds(P * C)
+    R = int(np.max(np.diff(b)))
+    return b, (lambda q: (q % C) * P + q // C), R
+
+
+@pytest.mark.parametrize("name,P,C", [("pubmed", 2, 3), ("arxiv", 2, 2), ("cora", 3, 4)])
+def test_chunked_partitions_simulated_on_one_gpu(gsp, name, P, C):
+    """Every (rank, chunk) partition runs on one GPU, each writing its [R, F] block
+    straight into its chunk's all-gather range [c*P*R, (c+1)*P*R) of the padded
+    table (the NCCL all-gather replaced by the output placement).  Un-padded:
+    == the oracle, element by element, for the three norms.  Reverse: symmetric
+    graphs over the shared topology (own rows), directed graphs as per-source
+    partials summed over all partitions (the reduce-scatter)."""
+    V, src, dst = datagen.make_graph(name)
+    G, og = graph_pair(gsp, V, src, dst)
+    F = 16
+    Xh = datagen.uniform(11, V, F)
+    b, slot, R = chunk_layout(G, P, C)
+    Q = P * C
+    parts = {(p, c): G.partition(P, p, device=0, nchunks=C, chunk=c) for p in range(P) for c in range(C)}
+    Xpad = torch.zeros((Q * R, F), device="cuda")
+    for q in range(Q):
+        Xpad[slot(q) * R:slot(q) * R + b[q + 1] - b[q]] = dev(Xh[b[q]:b[q + 1]])
+
+    def unpad(t):
+        g = t.cpu().numpy()
+        return np.concatenate([g[slot(q) * R:slot(q) * R + b[q + 1] - b[q]] for q in range(Q)])
+
+    for norm in NORMS:
+        full, T = og.gspmm(Xh, norm, False)
+        table = torch.full((Q * R, F), float("nan"), device="cuda")
+        for (p, c), pg in parts.items():
+            assert pg.row_base == slot(p * C + c) * R
+            pg.gspmm(Xpad, norm, out=table[(c * P + p) * R:(c * P + p + 1) * R])
+        assert_within(unpad(table), full, T, f"{name} chunked fwd n{norm}")
+        ref_r, Tr = og.gspmm(Xh, norm, True)
+        if G.symmetric:
+            table.fill_(float("nan"))
+            for (p, c), pg in parts.items():
+                pg.gspmm(Xpad, norm, out=table[(c * P + p) * R:(c * P + p + 1) * R], reverse=True)
+            assert_within(unpad(table), ref_r, Tr, f"{name} chunked sym rev n{norm}")
+        else:
+            acc = torch.zeros((Q * R, F), dtype=torch.float64, device="cuda")
+            for pg in parts.values():
+                assert pg.reverse_gives_partials()
+                acc += pg.gspmm(Xpad, norm, reverse=True).double()
+            assert_within(unpad(acc), ref_r, Tr, f"{name} chunked partial rev n{norm}")
+
+
+def test_chunked_partition_gat_forward(gsp):
+    """The fused GAT forward on chunked partitions reads its destination rows at
+    row_base + r of the padded table; local edge ids are the block's global range."""
+    cfg = datagen.CONFIGS["pubmed"]
+    V, src, dst = datagen.make_graph(cfg)
+    G, og = graph_pair(gsp, V, src, dst)
+    H, F, P, C = 8, 64, 2, 2
+    Zh = datagen.uniform(21, V, F)
+    b, slot, R = chunk_layout(G, P, C)
+    Zpad = torch.zeros((P * C * R, F), device="cuda")
+    for q in range(P * C):
+        Zpad[slot(q) * R:slot(q) * R + b[q + 1] - b[q]] = dev(Zh[b[q]:b[q + 1]])
+    a_ref, o_ref, T = og.gat_forward(Zh, Zh, Zh, H)
+    for p in range(P):
+        for c in range(C):
+            q = p * C + c
+            pg = G.partition(P, p, device=0, nchunks=C, chunk=c)
+            e0, e1 = og.fwd_off[b[q]], og.fwd_off[b[q + 1]]
+            alpha, out = pg.gat_forward(Zpad, Zpad, Zpad, H)
+            n = b[q + 1] - b[q]
+            assert_within(alpha.cpu().numpy(), a_ref[e0:e1], 1.0, "chunk alpha")
+            assert_within(out.cpu().numpy()[:n], o_ref[b[q]:b[q + 1]], T[b[q]:b[q + 1]], "chunk gat out")
+
+
+# ---------------------------------------------------- GCN-lean device format
+@pytest.mark.parametrize("name", ["pubmed", "arxiv"])
+def test_no_edge_ids_graph(gsp, name):
+    """GSP_BUILD_NO_EDGE_IDS (P:2012 "For GCN, GraphPy need only (|V|+|E|)"): a
+    symmetric graph holds one topology (8(V+1) + 4E bytes), a directed one two;
+    no edge-id bytes; gSpMMv in both directions still matches the oracle; the
+    edge-ID indirected reverse reports GSP_ERR_NO_REVERSE."""
+    V, src, dst = datagen.make_graph(name)
+    G = gsp.Graph(V, src, dst, device=0, edge_ids=False, edge_scales=False)
+    og = oracle.Graph(V, src, dst)
+    m = G.memory()
+    per = 8 * (V + 1) + 4 * og.E
+    assert m["topology"] == (per if G.symmetric else 2 * per)
+    assert m["edge_ids"] == 0 and m["edge_scales"] == 0
+    assert sum(m.values()) == G.device_bytes
+    assert m["vertex_arrays"] < 64 * V          # O(V): scales + schedules
+    Xh = datagen.uniform(4, V, 32)
+    for norm in NORMS:
+        for rev in (0, 1):
+            ref, T = og.gspmm(Xh, norm, bool(rev))
+            assert_within(G.gspmm(dev(Xh), norm, reverse=rev).cpu().numpy(), ref, T, f"lean n{norm} r{rev}")
+    w = torch.rand((og.E, 1), device="cuda")
+    with pytest.raises(gsp.GspError) as ei:
+        G.gspmm_weighted(dev(Xh), w, reverse=True)
+    assert ei.value.name == "GSP_ERR_NO_REVERSE"
+    # the default graph: edge ids and (on request) per-edge scales are accounted separately
+    Gd = gsp.Graph(V, src, dst, device=0, edge_scales=True)
+    md = Gd.memory()
+    assert md["edge_ids"] == 4 * og.E and md["edge_scales"] == 4 * og.E * (1 if Gd.symmetric else 2)
+    assert sum(md.values()) == Gd.device_bytes
+
+
+# ------------------------------------------------ aliasing of strided views
+def test_alias_exact_for_column_slices(gsp):
+    """Disjoint column slices of one buffer are not aliases (exact strided test);
+    interleaving or overlapping ones are; broadcast rows are rejected."""
+    V, src, dst = datagen.make_graph("cora")
+    G, og = graph_pair(gsp, V, src, dst)
+    F = 8
+    Xh = datagen.uniform(5, V, F)
+    B = torch.zeros((V, 2 * F), device="cuda")
+    B[:, :F] = dev(Xh)
+    G.gspmm(B[:, :F], gsp.NORM_BOTH, out=B[:, F:])
+    ref, T = og.gspmm(Xh, gsp.NORM_BOTH, False)
+    assert_within(B[:, F:].cpu().numpy(), ref, T, "column-slice out")
+    with pytest.raises(gsp.GspError) as ei:
+        G.gspmm(B[:, :F], gsp.NORM_BOTH, out=B[:, F // 2:F // 2 + F])
+    assert ei.value.name == "GSP_ERR_ALIAS"
+    C = torch.zeros((V + 1, F), device="cuda")
+    with pytest.raises(gsp.GspError) as ei:      # rows shifted by one: overlapping
+        G.gspmm(C[:V], gsp.NORM_BOTH, out=C[1:])
+    assert ei.value.name == "GSP_ERR_ALIAS"
+    with pytest.raises(ValueError):
+        G.gspmm(torch.zeros(F, device="cuda").expand(V, F), gsp.NORM_BOTH)
+
+
+# ------------------------------------- SURVEY L18: margin of approximate exp
+def test_approx_exp_paths_keep_10x_margin(gsp, golden):
+    """the kernels' exp is ex2.approx (edge softmax, fused GAT
+    forward); allowed only if parity holds with >= 10x margin, i.e. max
+    err/bound <= 0.1 on T4 / D4 / random graphs (brute-force sizes) and Pubmed."""
+    graphs = []
+    for gf in ("t4.json", "d4.json"):
+        g = golden(gf)
+        graphs.append((gf, g["V"], np.array(g["src"], np.int64), np.array(g["dst"], np.int64)))
+    for seed in range(6):
+        rng = np.random.default_rng(900 + seed)
+        V = int(rng.integers(2, 64)) if seed < 3 else int(rng.integers(200, 3000))
+        E = int(rng.integers(1, 40 * V))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed % 2 == 0
+                    else datagen.skewed_multigraph(V, E, seed, alpha=1.5))
+        graphs.append((f"random{seed}", V, src, dst))
+    graphs.append(("pubmed",) + datagen.make_graph("pubmed"))
+    worst = {"edge_softmax": 0.0, "gat_fused_alpha": 0.0, "gat_fused_out": 0.0}
+    for name, V, src, dst in graphs:
+        G, og = graph_pair(gsp, V, src, dst)
+        for H in (1, 4, 8):
+            lh = datagen.uniform(V + H, og.E, H, lo=-8, hi=8)
+            r = assert_within(G.edge_softmax(dev(lh)).cpu().numpy(), og.edge_softmax(lh), 1.0, f"{name} sm H{H}")
+            worst["edge_softmax"] = max(worst["edge_softmax"], r)
+        for H in (2, 8):     # the fused (one pass) kernel: Fh = 8
+            Zh = datagen.uniform(V + 7 * H, V, 8 * H)
+            Vh = datagen.uniform(V + 9 * H, V, 8 * H)
+            a_ref, o_ref, T = og.gat_forward(Zh, Zh, Vh, H)
+            alpha, out = G.gat_forward(dev(Zh), dev(Zh), dev(Vh), H)
+            worst["gat_fused_alpha"] = max(worst["gat_fused_alpha"],
+                                           assert_within(alpha.cpu().numpy(), a_ref, 1.0, f"{name} a H{H}"))
+            worst["gat_fused_out"] = max(worst["gat_fused_out"],
+                                         assert_within(out.cpu().numpy(), o_ref, T, f"{name} out H{H}"))
+    print("approx-exp margins (max err/bound):", worst)
+    for k, v in worst.items():
+        assert v <= 0.1, f"{k}: max err/bound {v:.3g} > 0.1 (SURVEY L18 10x margin)"

@@ -603,3 +603,67 @@ def test_rows_coo_matches_full_oracle(seed):
         assert first == G.fwd_off[v]
         assert np.array_equal(pairs[:, 0], G.fwd_col[G.fwd_off[v]:G.fwd_off[v + 1]])
         assert np.array_equal(G.coo_to_eid[pairs[:, 1]], np.arange(G.fwd_off[v], G.fwd_off[v + 1]))
+
+
+# ------------------------------- C14 / C15 additive GAT attention (NEXT-3)
+def test_gsddmm_add_leaky_t4_golden(golden):
+    g, c = golden("t4.json"), golden("t4_additive.json")
+    G = oracle.Graph(g["V"], g["src"], g["dst"])
+    el = np.array(c["el"], np.float32)[:, None]
+    er = np.array(c["er"], np.float32)[:, None]
+    assert np.allclose(G.gsddmm_add_leaky(el, er, c["slope"])[:, 0], c["scores"], rtol=1e-15, atol=1e-15)
+    assert G.gsddmm_add_leaky(el, er, 1.0)[:, 0].tolist() == c["scores_slope1"]
+
+
+@pytest.mark.parametrize("seed", range(15))
+def test_gsddmm_add_leaky_bruteforce(seed):
+    """Brute force from the COO list (per input edge i: lrelu(el[src_i] + er[dst_i]),
+    placed at its edge ID); slope 1 == C13's u_add_v as two gSDDMMve calls."""
+    V, src, dst = rand_graph(14000 + seed)
+    G = oracle.Graph(V, src, dst)
+    H = 1 + seed % 4
+    el = datagen.uniform(seed, V, H, lo=-3, hi=3)
+    er = datagen.uniform(seed + 1, V, H, lo=-3, hi=3)
+    slope = [0.2, 0.01, 0.5][seed % 3]
+    x = el[src].astype(np.float64) + er[dst].astype(np.float64)
+    ref = np.zeros((G.E, H))
+    ref[G.coo_to_eid] = np.where(x > 0, x, slope * x)
+    assert np.array_equal(G.gsddmm_add_leaky(el, er, slope), ref)
+    if G.E:
+        zero = np.zeros((G.E, H), np.float32)
+        dst_side = G.gsddmm_ve(er, zero, oracle.OP_ADD, 0).astype(np.float32)
+        both = G.gsddmm_ve(el, dst_side, oracle.OP_ADD, 1)
+        assert np.array_equal(G.gsddmm_add_leaky(el, er, 1.0), both)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_gat_forward_additive_bruteforce(seed):
+    """C15 against a per-destination brute force over the COO list (scores,
+    scipy softmax, weighted sum of Vt[src]) and against the composition
+    C5(C7(C14)) of pinned components; alpha rows sum to 1."""
+    V, src, dst = rand_graph(15000 + seed)
+    G = oracle.Graph(V, src, dst)
+    H = [1, 2, 4][seed % 3]
+    Fvh = 1 + seed % 3
+    el = datagen.uniform(seed, V, H, lo=-4, hi=4)
+    er = datagen.uniform(seed + 1, V, H, lo=-4, hi=4)
+    Vt = datagen.uniform(seed + 2, V, H * Fvh)
+    a, out, T = G.gat_forward_additive(el, er, Vt, 0.2)
+    ref_a = np.zeros((G.E, H))
+    ref_o = np.zeros((V, H * Fvh))
+    for v in range(V):
+        idx = np.nonzero(dst == v)[0]
+        if idx.size == 0:
+            continue
+        x = el[src[idx]].astype(np.float64) + er[v].astype(np.float64)
+        sc = np.where(x > 0, x, 0.2 * x)
+        al = scipy.special.softmax(sc, axis=0)                    # [deg, H]
+        ref_a[G.coo_to_eid[idx]] = al
+        ref_o[v] = (np.repeat(al, Fvh, axis=1) * Vt[src[idx]].astype(np.float64)).sum(0)
+    assert np.allclose(a, ref_a, atol=1e-13)
+    check(out, T, ref_o)
+    s = G.gsddmm_add_leaky(el, er, 0.2)
+    a2 = G.edge_softmax(s.astype(np.float32))
+    assert np.allclose(a, a2, atol=2e-6)
+    o2, _ = G.gspmm_weighted(Vt, a2.astype(np.float32))
+    assert np.all(np.abs(out - o2) <= 1e-5 * (T + 1))
