@@ -262,6 +262,32 @@ gsp_status gsp_gspmm_e(const gsp_graph *g, const gsp_tensor *w, int reduce, gsp_
 gsp_status gsp_gsddmm_ve(const gsp_graph *g, const gsp_tensor *X, const gsp_tensor *w, int op, int side,
                          gsp_tensor *out, gsp_stream stream);
 
+/* Additive GAT attention scores (NEXT-3; the u_add_v form of Table 1's gSDDMM
+ * family, P:562-568 / P:1329-1331, followed by the standard GAT leaky ReLU,
+ * SPEC S:380 "edge logit = leaky_relu(<a_src, z[.]> + <a_dst, z[.]>, slope)",
+ * slope 0.2 at S:411).  For slot j of fwd row v with column (source) u_j:
+ *   out[j, h] = lrelu(el[u_j, h] + er[v, h]),  lrelu(x) = x > 0 ? x : slope * x
+ * el = source-side, er = destination-side per-head vertex scalars, both
+ * [ncols, H] (partitions: the padded tables, er read at row row_base + r);
+ * out [E, H] by edge ID.  fp32 add and multiply (oracle C14 in fp64).
+ * Errors: NULL, ARG (non-finite slope, host-only graph), SHAPE, ALIAS (out
+ * overlapping el or er), CUDA. */
+gsp_status gsp_gsddmm_add_leaky(const gsp_graph *g, const gsp_tensor *el, const gsp_tensor *er, float slope,
+                                gsp_tensor *out, gsp_stream stream);
+
+/* Fused additive GAT forward (NEXT-3 + NEXT-2; oracle C15): the standard GAT
+ * layer's attention and aggregation in one pass per destination row, alpha
+ * still materialised:
+ *   alpha = edge_softmax(gsddmm_add_leaky(el, er, slope))   [E, H] by edge ID
+ *   out   = gspmm_weighted(Vt, alpha)                         [nrows, Vt->cols]
+ * One pass (online softmax) when Vt->cols = 8 H, H in {2, 4, 8, 16},
+ * alpha->ld == H and a 32-byte aligned Vt; else the three kernels in sequence.
+ * 1 <= H <= 16.  Errors: NULL, ARG, SHAPE, ALIAS (out or alpha overlapping an
+ * input, out overlapping alpha), CUDA. */
+gsp_status gsp_gat_forward_additive(const gsp_graph *g, const gsp_tensor *el, const gsp_tensor *er,
+                                    const gsp_tensor *Vt, float slope, gsp_tensor *alpha, gsp_tensor *out,
+                                    gsp_stream stream);
+
 /* -------------------------------------------------------------- multi-GPU */
 
 /* Edge-balanced contiguous row bounds:

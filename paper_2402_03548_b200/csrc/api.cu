@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -707,6 +708,103 @@ gsp_status gsp_gat_backward_scores(const gsp_graph *g, const gsp_tensor *dOut, c
         }
     }
     if (e != cudaSuccess) return cuda_fail(e, "gat_backward_scores launch");
+    return GSP_OK;
+}
+
+// ------------------------------------- NEXT-3: additive GAT attention (C14, C15)
+static gsp_status check_additive(const gsp_graph *g, const gsp_tensor *el, const gsp_tensor *er, float slope,
+                                 int64_t *H) {
+    gsp_status st;
+    const gsp::DevStructure &S = g->fwd;
+    if (!S.present) return fail(GSP_ERR_ARG, "needs the fwd structure (not a reverse partition)");
+    if (!el || !er) return fail(GSP_ERR_NULL, "el/er is NULL");
+    if (!std::isfinite(slope)) return fail(GSP_ERR_ARG, "slope must be finite");
+    if ((st = check_tensor(g, el, "el", S.ncols, -1)) != GSP_OK) return st;
+    if ((st = check_tensor(g, er, "er", S.ncols, el->cols)) != GSP_OK) return st;
+    *H = el->cols;
+    if (*H < 1) return fail(GSP_ERR_SHAPE, "el/er must have H >= 1 columns");
+    return GSP_OK;
+}
+
+gsp_status gsp_gsddmm_add_leaky(const gsp_graph *g, const gsp_tensor *el, const gsp_tensor *er, float slope,
+                                gsp_tensor *out, gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    int64_t H = 0;
+    if ((st = check_additive(g, el, er, slope, &H)) != GSP_OK) return st;
+    if (!out) return fail(GSP_ERR_NULL, "out is NULL");
+    if ((st = check_tensor(g, out, "out", g->E, H)) != GSP_OK) return st;
+    if (overlaps(out, el) || overlaps(out, er)) return fail(GSP_ERR_ALIAS, "out overlaps el or er");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    const gsp::DevStructure &S = g->fwd;
+    gsp::SddmmAddArgs a{};
+    a.off = S.off; a.col = S.col; a.order = S.order; a.task = S.task; a.nrows = S.nrows; a.n_heavy = S.n_heavy;
+    a.row_base = g->row_base;
+    a.el = static_cast<const float *>(el->data); a.lde = el->ld;
+    a.er = static_cast<const float *>(er->data); a.ldr = er->ld;
+    a.out = static_cast<float *>(out->data); a.ldo = out->ld;
+    a.H = H; a.slope = slope;
+    cudaError_t e = gsp::launch_sddmm_add(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gsddmm_add_leaky launch");
+    return GSP_OK;
+}
+
+gsp_status gsp_gat_forward_additive(const gsp_graph *g, const gsp_tensor *el, const gsp_tensor *er,
+                                    const gsp_tensor *Vt, float slope, gsp_tensor *alpha, gsp_tensor *out,
+                                    gsp_stream stream) {
+    gsp_status st;
+    if ((st = check_compute_graph(g)) != GSP_OK) return st;
+    int64_t H = 0;
+    if ((st = check_additive(g, el, er, slope, &H)) != GSP_OK) return st;
+    if (!Vt || !alpha || !out) return fail(GSP_ERR_NULL, "Vt/alpha/out is NULL");
+    const gsp::DevStructure &S = g->fwd;
+    if (H > 16) return fail(GSP_ERR_SHAPE, "1 <= H <= 16 heads");
+    if ((st = check_tensor(g, alpha, "alpha", g->E, H)) != GSP_OK) return st;
+    if ((st = check_tensor(g, Vt, "Vt", S.ncols, -1)) != GSP_OK) return st;
+    if (Vt->cols % H != 0) return fail(GSP_ERR_SHAPE, "Vt.cols must be a multiple of H");
+    if ((st = check_tensor(g, out, "out", S.nrows, Vt->cols)) != GSP_OK) return st;
+    if (overlaps(out, el) || overlaps(out, er) || overlaps(out, Vt) || overlaps(out, alpha))
+        return fail(GSP_ERR_ALIAS, "out overlaps an input or alpha");
+    if (overlaps(alpha, el) || overlaps(alpha, er) || overlaps(alpha, Vt))
+        return fail(GSP_ERR_ALIAS, "alpha overlaps el, er or Vt");
+    if ((st = check_stream(g, stream)) != GSP_OK) return st;
+    DeviceGuard dg(g->device);
+    cudaStream_t cs = (cudaStream_t)stream;
+    gsp::GatArgs ga{};
+    ga.off = S.off; ga.col = S.col; ga.order = S.order; ga.task = S.task; ga.nrows = S.nrows; ga.n_heavy = S.n_heavy;
+    ga.row_base = g->row_base;
+    ga.X = static_cast<const float *>(er->data); ga.ldx = er->ld;
+    ga.Y = static_cast<const float *>(el->data); ga.ldy = el->ld;
+    ga.Vt = static_cast<const float *>(Vt->data); ga.ldv = Vt->ld;
+    ga.alpha = static_cast<float *>(alpha->data);
+    ga.out = static_cast<float *>(out->data); ga.ldo = out->ld;
+    ga.H = H; ga.additive = 1; ga.slope = slope;
+    cudaError_t e;
+    if (Vt->cols == 8 * H && alpha->ld == H && gsp::gat_fused_supported(ga)) {
+        e = gsp::launch_gat_fused(ga, cs);
+    } else {   // any other shape: scores, softmax in place, weighted aggregate (same results within the bound)
+        gsp::SddmmAddArgs sa{};
+        sa.off = S.off; sa.col = S.col; sa.order = S.order; sa.task = S.task; sa.nrows = S.nrows;
+        sa.n_heavy = S.n_heavy; sa.row_base = g->row_base;
+        sa.el = ga.Y; sa.lde = el->ld; sa.er = ga.X; sa.ldr = er->ld;
+        sa.out = ga.alpha; sa.ldo = alpha->ld; sa.H = H; sa.slope = slope;
+        e = gsp::launch_sddmm_add(sa, cs);
+        if (e == cudaSuccess) {
+            gsp::SoftmaxArgs xa{};
+            xa.off = S.off; xa.order = S.order; xa.task = S.task; xa.nrows = S.nrows; xa.n_heavy = S.n_heavy;
+            xa.e = ga.alpha; xa.lde = alpha->ld; xa.out = ga.alpha; xa.ldo = alpha->ld; xa.H = H;
+            e = gsp::launch_softmax(xa, cs);
+        }
+        if (e == cudaSuccess) {
+            gsp::SpmmArgs wa{};
+            wa.off = S.off; wa.col = S.col; wa.order = S.order; wa.task = S.task; wa.nrows = S.nrows; wa.n_heavy = S.n_heavy;
+            wa.X = ga.Vt; wa.ldx = Vt->ld; wa.out = ga.out; wa.ldo = out->ld; wa.F = Vt->cols;
+            wa.w = ga.alpha; wa.ldw = alpha->ld; wa.H = H; wa.Fh = Vt->cols / H > 0 ? Vt->cols / H : 1;
+            e = gsp::launch_spmm(wa, gsp::kSpmmWeightedFwd, cs);
+        }
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "gat_forward_additive launch");
     return GSP_OK;
 }
 

@@ -20,12 +20,19 @@ namespace {
 // in-flight score blocks no longer crowd the gathered table out of L2.  Y and
 // Vt may be the same table (one gather serves both).  Heavy rows: CTA split +
 // deterministic merge.
-template <int LPE, bool SAME>
-__global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a) {
+// MODE 0: s = <X[v,h], Y[u,h]>, Vt == Y (one gather); MODE 1: the same with a
+// separate Vt; MODE 2 (NEXT-3, oracle C15): additive attention
+// s = lrelu(Y[u,h] + X[v,h], slope) with Y = el, X = er one float per head
+// ([ncols, H] tables) -- the standard GAT logit.
+template <int LPE, int MODE, int UOVR = 0, int MINB = 2>
+__global__ void __launch_bounds__(kThreads, MINB) gat_fused_kernel(const GatArgs a) {
     constexpr int VEC = 8;
     constexpr int G = 32 / LPE;
     constexpr int PER = LPE;
-    constexpr int U = SAME ? (PER >= 8 ? 8 : PER) : (PER >= 4 ? 4 : PER);   // edges in flight per lane
+    constexpr bool SAME = MODE == 0, ADD = MODE == 2;
+    constexpr int XV = ADD ? 1 : VEC;    // floats of the score operands per lane
+    constexpr int U0 = UOVR ? UOVR : ((SAME || ADD) ? 8 : 4);
+    constexpr int U = U0 > PER ? PER : U0;   // edges in flight per lane
     __shared__ __align__(16) int s_col[kWarps][32];
     // running Kahan state (acc, accc) per lane lives in smem: touched once per
     // tile (fold) and on the rare max increase (rescale), keeping registers for
@@ -45,9 +52,9 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
     const int64_t cap = a.sc_cap;
     float *wsc = s_sc + (int64_t)warp * cap * LPE;
 
-    Vec<VEC> xv;
-    ld_keep(xv, a.X + (a.row_base + row) * a.ldx + h * VEC, pol.stream);
-    const char *yl = reinterpret_cast<const char *>(a.Y + h * VEC);
+    Vec<XV> xv;
+    ld_keep(xv, a.X + (a.row_base + row) * a.ldx + h * XV, pol.stream);
+    const char *yl = reinterpret_cast<const char *>(a.Y + h * XV);
     const char *vl = reinterpret_cast<const char *>(a.Vt + h * VEC);
     const uint32_t ldyb = (uint32_t)(a.ldy * 4), ldvb = (uint32_t)(a.ldv * 4);
 
@@ -77,7 +84,8 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
         const int mcount = n == 32 ? PER : (n > g ? (n - g + G - 1) / G : 0);
         auto body = [&](int i, auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
-            Vec<VEC> y[U], vv[SAME ? 1 : U];
+            Vec<XV> y[U];
+            Vec<VEC> vv[SAME ? 1 : U];
             int cc[U];
             if constexpr (U % 4 == 0) {
 #pragma unroll
@@ -105,13 +113,18 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
             float mb = -INFINITY;
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                float s0 = 0.f, s1 = 0.f;   // two chains: shorter dependency
+                if constexpr (ADD) {
+                    const float x = y[u].v[0] + xv.v[0];
+                    sc[u] = x > 0.f ? x : a.slope * x;
+                } else {
+                    float s0 = 0.f, s1 = 0.f;   // two chains: shorter dependency
 #pragma unroll
-                for (int t = 0; t < VEC; t += 2) {
-                    s0 = fmaf(xv.v[t], y[u].v[t], s0);
-                    s1 = fmaf(xv.v[t + 1], y[u].v[t + 1], s1);
+                    for (int t = 0; t < VEC; t += 2) {
+                        s0 = fmaf(xv.v[t], y[u].v[t], s0);
+                        s1 = fmaf(xv.v[t + 1], y[u].v[t + 1], s1);
+                    }
+                    sc[u] = s0 + s1;
                 }
-                sc[u] = s0 + s1;
                 if (FULL || i + u < mcount) {
                     ab[(int64_t)(G * (i + u)) * H] = sc[u];   // raw score (smem, or global with the default L2 policy)
                     mb = fmaxf(mb, sc[u]);
@@ -137,10 +150,14 @@ __global__ void __launch_bounds__(kThreads, 2) gat_fused_kernel(const GatArgs a)
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const float pu = fast_exp(sc[u] - m);   // 0 for padding (-inf)
-                const Vec<VEC> &val = SAME ? y[u] : vv[SAME ? 0 : u];
                 St += pu;
+                if constexpr (SAME) {
 #pragma unroll
-                for (int t = 0; t < VEC; t++) acct.v[t] = fmaf(pu, val.v[t], acct.v[t]);
+                    for (int t = 0; t < VEC; t++) acct.v[t] = fmaf(pu, y[u].v[t], acct.v[t]);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < VEC; t++) acct.v[t] = fmaf(pu, vv[u].v[t], acct.v[t]);
+                }
             }
         };
         if (n == 32) {
@@ -398,8 +415,10 @@ __global__ void __launch_bounds__(kThreads, 2) gat_bwd_kernel(const GatArgs a) {
 bool gat_fused_supported(const GatArgs &a) {
     const int64_t H = a.H;
     const bool h_ok = H == 2 || H == 4 || H == 8 || H == 16 || H == 32;
-    return h_ok && a.ldx % 8 == 0 && a.ldy % 8 == 0 && a.ldv % 8 == 0 && a.ldo % 4 == 0 && aligned(a.X, 32) &&
-           aligned(a.Y, 32) && aligned(a.Vt, 32) && aligned(a.out, 16) && aligned(a.alpha, 16);
+    const bool xy_ok = a.additive ? (aligned(a.X, 4) && aligned(a.Y, 4))
+                                  : (a.ldx % 8 == 0 && a.ldy % 8 == 0 && aligned(a.X, 32) && aligned(a.Y, 32));
+    return h_ok && xy_ok && a.ldv % 8 == 0 && a.ldo % 4 == 0 && aligned(a.Vt, 32) && aligned(a.out, 16) &&
+           aligned(a.alpha, 16);
 }
 
 // shared-memory score block per warp (bytes); GSP_GAT_SMEM_KB overrides (0: off, A/B)
@@ -431,7 +450,7 @@ cudaError_t opt_in_smem(K kernel, size_t dyn, AttrFlags &flags) {
     }
     return cudaSuccess;
 }
-template <int HH, bool SAME>
+template <int HH, int MODE, int UO, int MB>
 AttrFlags &gat_fused_attr() {
     static AttrFlags f{};
     return f;
@@ -442,28 +461,54 @@ AttrFlags &gat_bwd_attr() {
     return f;
 }
 
-template <int HH, bool SAME>
-cudaError_t launch_gat_h(GatArgs a, dim3 grid, cudaStream_t s) {
+template <int HH, int MODE, int UO = 0, int MB = 2>
+cudaError_t launch_gat_v(GatArgs a, dim3 grid, cudaStream_t s) {
     a.sc_cap = (gat_score_bytes() / (4 * HH)) & ~int64_t(31);   // whole 32-edge tiles
     const size_t dyn = (size_t)(kWarps * a.sc_cap * HH * 4);
-    cudaError_t e = opt_in_smem(gat_fused_kernel<HH, SAME>, dyn, gat_fused_attr<HH, SAME>());
+    cudaError_t e = opt_in_smem(gat_fused_kernel<HH, MODE, UO, MB>, dyn, gat_fused_attr<HH, MODE, UO, MB>());
     if (e != cudaSuccess) return e;
-    gat_fused_kernel<HH, SAME><<<grid, kThreads, dyn, s>>>(a);
+    gat_fused_kernel<HH, MODE, UO, MB><<<grid, kThreads, dyn, s>>>(a);
     return cudaGetLastError();
+}
+
+// tuning knob for H = 8 (GSP_TUNE_GAT: (edges in flight per lane, CTAs per SM)); read once
+static int tune_gat() {
+    static int v = [] {
+        const char *e = getenv("GSP_TUNE_GAT");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
+template <int HH, int MODE>
+cudaError_t launch_gat_h(GatArgs a, dim3 grid, cudaStream_t s) {
+    if constexpr (HH == 8) {
+        switch (tune_gat()) {
+            case 1: return launch_gat_v<HH, MODE, 4, 3>(a, grid, s);
+            case 2: return launch_gat_v<HH, MODE, 4, 2>(a, grid, s);
+            case 3: return launch_gat_v<HH, MODE, 2, 4>(a, grid, s);
+            case 4: return launch_gat_v<HH, MODE, 8, 3>(a, grid, s);
+            default: break;
+        }
+    }
+    return launch_gat_v<HH, MODE>(a, grid, s);
 }
 
 cudaError_t launch_gat_fused(const GatArgs &a, cudaStream_t s) {
     if (a.nrows == 0) return cudaSuccess;
     const dim3 grid = row_grid(a.nrows, a.n_heavy, 1);
-    const bool same = a.Vt == a.Y && a.ldv == a.ldy;
-#define GSP_GAT_CASE(HH) \
-    case HH: return same ? launch_gat_h<HH, true>(a, grid, s) : launch_gat_h<HH, false>(a, grid, s);
+    const int mode = a.additive ? 2 : ((a.Vt == a.Y && a.ldv == a.ldy) ? 0 : 1);
+#define GSP_GAT_CASE(HH)                                                      \
+    case HH:                                                                  \
+        return mode == 0 ? launch_gat_h<HH, 0>(a, grid, s)                    \
+                         : (mode == 1 ? launch_gat_h<HH, 1>(a, grid, s) : launch_gat_h<HH, 2>(a, grid, s));
     switch (a.H) {
         GSP_GAT_CASE(2)
         GSP_GAT_CASE(4)
         GSP_GAT_CASE(8)
         GSP_GAT_CASE(16)
-        default: return same ? launch_gat_h<32, true>(a, grid, s) : launch_gat_h<32, false>(a, grid, s);
+        GSP_GAT_CASE(32)
+        default: return cudaErrorNotSupported;
     }
 #undef GSP_GAT_CASE
 }

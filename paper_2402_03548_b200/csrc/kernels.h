@@ -26,6 +26,7 @@ struct SpmmArgs {
     int64_t ldw;
     int64_t H, Fh;
     int pf;                  // L2 prefetch distance of the edge streams, in 32-edge tiles (0 = off)
+    int wpol;                // L2 policy of the weight rows: 0 evict_first (streamed once), 1 evict_normal, 2 evict_last
     int out_vec;             // out rows 16-B aligned (ldo % 4 == 0): vector stores, else scalar (set by launch_spmm)
 };
 
@@ -99,6 +100,8 @@ struct GatArgs {
     int64_t ldo;
     int64_t H;
     int64_t sc_cap;    // edges per warp slice whose raw scores stay in shared memory (set by the launcher)
+    int additive;      // 0: scores <X[v], Y[u]> (Fh = 8); 1: lrelu(Y[u,h] + X[v,h], slope) (X = er, Y = el: [ncols, H])
+    float slope;
 };
 bool gat_fused_supported(const GatArgs &a);
 cudaError_t launch_gat_fused(const GatArgs &a, cudaStream_t s);
@@ -138,6 +141,24 @@ struct SddmmVeArgs {
     int side_src;            // 1: X indexed by the column (source), 0: by the row (destination)
 };
 cudaError_t launch_sddmm_ve(const SddmmVeArgs &a, cudaStream_t s);
+
+// NEXT-3 additive GAT scores (oracle C14): out[j,h] = lrelu(el[col_j,h] + er[row_base+row,h], slope)
+struct SddmmAddArgs {
+    const int64_t *off;
+    const int32_t *col;
+    const int32_t *order;
+    const int32_t *task;
+    int64_t nrows, n_heavy, row_base;
+    const float *el;         // source side [ncols, H]
+    int64_t lde;
+    const float *er;         // destination side [ncols, H]
+    int64_t ldr;
+    float *out;              // [E, H]
+    int64_t ldo;
+    int64_t H;
+    float slope;
+};
+cudaError_t launch_sddmm_add(const SddmmAddArgs &a, cudaStream_t s);
 
 // out[j] = scale[col[j]] for j < nnz (per-edge column scales, built once at create)
 cudaError_t launch_gather_scale(const int32_t *col, int64_t nnz, const float *scale, float *out, cudaStream_t s);

@@ -209,6 +209,61 @@ cudaError_t sddmm_ve_op(const SddmmVeArgs &a, cudaStream_t s) {
     }
 }
 
+// ============================================ NEXT-3: additive GAT scores
+// out[j, h] = lrelu(el[u_j, h] + er[v, h]) (oracle C14; P:1329-1331 gSDDMM
+// family, SPEC S:380 / S:411 additive attention with leaky ReLU): el is the
+// source-side table, er the destination side (padded tables on partitions:
+// er row row_base + r).  Scalar path: lanes stride over the row's (edge, head)
+// pairs; vector path (H in {4, 8, 16, 32}, 16-B rows): QH = H/4 lanes per
+// edge, one float4 of heads each, 4 edges in flight per lane, er[v] loaded
+// once per lane; the score stream is written evict_first.
+__device__ __forceinline__ float lrelu(float x, float slope) { return x > 0.f ? x : slope * x; }
+
+__global__ void __launch_bounds__(kThreads) sddmm_add_kernel(const SddmmAddArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t idx = (int64_t)blockIdx.x * kWarps + warp;
+    if (idx >= a.nrows) return;
+    const int64_t row = a.order[idx], b = a.off[row], e = a.off[row + 1];
+    const int64_t H = a.H;
+    for (int64_t t = lane; t < (e - b) * H; t += 32) {
+        const int64_t j = b + t / H, h = t % H;
+        const float x = __ldg(a.el + (int64_t)__ldg(a.col + j) * a.lde + h) + __ldg(a.er + (a.row_base + row) * a.ldr + h);
+        a.out[j * a.ldo + h] = lrelu(x, a.slope);
+    }
+}
+
+template <int QH>
+__global__ void __launch_bounds__(kThreads) sddmm_add_vec_kernel(const SddmmAddArgs a) {
+    constexpr int EPW = 32 / QH, U = 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t row, b, e;
+    bool heavy;
+    if (!warp_task(a.task, a.nrows, a.n_heavy, warp, row, b, e, heavy)) return;
+    const Pol pol = make_pol();
+    const int eo = lane / QH, q = lane % QH;
+    const float sl = a.slope;
+    const float4 r = b < e ? __ldg(reinterpret_cast<const float4 *>(a.er + (a.row_base + row) * a.ldr + 4 * q))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    auto one = [&](int64_t jj, const float4 x) {
+        st_stream_f4(a.out + jj * a.ldo + 4 * q,
+                     make_float4(lrelu(x.x + r.x, sl), lrelu(x.y + r.y, sl), lrelu(x.z + r.z, sl), lrelu(x.w + r.w, sl)),
+                     pol.stream);
+    };
+    int64_t j = b + eo;
+    for (; j + (U - 1) * EPW < e; j += U * EPW) {
+        int c[U];
+        float4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) c[u] = ld_stream_i32(a.col + j + u * EPW, pol.stream);
+#pragma unroll
+        for (int u = 0; u < U; u++) x[u] = __ldg(reinterpret_cast<const float4 *>(a.el + (int64_t)c[u] * a.lde + 4 * q));
+#pragma unroll
+        for (int u = 0; u < U; u++) one(j + u * EPW, x[u]);
+    }
+    for (; j < e; j += EPW)
+        one(j, __ldg(reinterpret_cast<const float4 *>(a.el + (int64_t)ld_stream_i32(a.col + j, pol.stream) * a.lde + 4 * q)));
+}
+
 int tune_sddmm() {
     static int v = [] {
         const char *e = getenv("GSP_TUNE_SDDMM");
@@ -296,6 +351,24 @@ cudaError_t launch_sddmm_ve(const SddmmVeArgs &a, cudaStream_t s) {
         case 16: return sddmm_ve_op<4>(a, s);
         default: return sddmm_ve_op<8>(a, s);
     }
+}
+
+cudaError_t launch_sddmm_add(const SddmmAddArgs &a, cudaStream_t s) {
+    if (a.nrows == 0 || a.H == 0) return cudaSuccess;
+    const bool vec = (a.H == 4 || a.H == 8 || a.H == 16 || a.H == 32) && a.lde % 4 == 0 && a.ldr % 4 == 0 &&
+                     a.ldo % 4 == 0 && aligned(a.el, 16) && aligned(a.er, 16) && aligned(a.out, 16);
+    if (!vec) {
+        sddmm_add_kernel<<<(unsigned)ceil_div(a.nrows, kWarps), kThreads, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    const dim3 grid = row_grid(a.nrows, a.n_heavy, 1);
+    switch (a.H) {
+        case 4: sddmm_add_vec_kernel<1><<<grid, kThreads, 0, s>>>(a); break;
+        case 8: sddmm_add_vec_kernel<2><<<grid, kThreads, 0, s>>>(a); break;
+        case 16: sddmm_add_vec_kernel<4><<<grid, kThreads, 0, s>>>(a); break;
+        default: sddmm_add_vec_kernel<8><<<grid, kThreads, 0, s>>>(a); break;
+    }
+    return cudaGetLastError();
 }
 
 }  // namespace gsp

@@ -132,9 +132,14 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
         }
         return 0.f;
     };
+    uint64_t wp = pol.stream;
+    if constexpr (W) {
+        if (a.wpol == 1) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(wp));
+        else if (a.wpol == 2) wp = pol.keep;
+    }
     auto load_w8 = [&](int64_t tb, int ev, float *d) {
         if constexpr (W) {
-            if (tb + lane < e) ld_stream_v8(d, a.w + (int64_t)ev * 8, pol.stream);
+            if (tb + lane < e) ld_stream_v8(d, a.w + (int64_t)ev * 8, wp);
             else {
 #pragma unroll
                 for (int t = 0; t < 8; t++) d[t] = 0.f;
@@ -567,10 +572,22 @@ static int prefetch_tiles() {
     return v;
 }
 
+// L2 policy of the edge-ID indirected weight rows of the weighted reverse (GSP_WREV_POL for A/B):
+// rev rows of one id window read runs of adjacent alpha rows in each destination's block,
+// so the rows are reused by the window's other sources
+static int wrev_policy() {
+    static int v = [] {
+        const char *e = getenv("GSP_WREV_POL");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 cudaError_t launch_spmm(const SpmmArgs &a_in, int mode, cudaStream_t s) {
     if (a_in.nrows == 0 || a_in.F == 0) return cudaSuccess;
     SpmmArgs a = a_in;
     a.pf = prefetch_tiles();
+    a.wpol = mode == kSpmmWeightedRev ? wrev_policy() : 0;
     const bool wmode = mode == kSpmmWeightedFwd || mode == kSpmmWeightedRev;
     if (wmode && a.H > kHMax) return cudaErrorNotSupported;   // api.cu rejects H > 16 first
     // the gather width depends on X only; an output stride that is not a multiple of 4

@@ -32,6 +32,7 @@ SYMBOLS = ["gsp_graph_create", "gsp_graph_destroy", "gsp_graph_info", "gsp_graph
            "gsp_gspmm_weighted", "gsp_gsddmm", "gsp_edge_softmax", "gsp_edge_softmax_backward",
            "gsp_gat_forward", "gsp_gat_backward_scores", "gsp_gspmm_reduce", "gsp_gspmm_e", "gsp_gsddmm_ve", "gsp_partition_bounds", "gsp_graph_partition",
            "gsp_graph_partition_chunked", "gsp_partition_chunk_info", "gsp_graph_memory",
+           "gsp_gsddmm_add_leaky", "gsp_gat_forward_additive",
            "gsp_partition_info", "gsp_status_string", "gsp_last_error_detail", "gsp_version"]
 
 
@@ -75,6 +76,8 @@ def _load():
         "gsp_graph_partition_chunked": ([p, ci, ci, ci, ci, ci, u32, P(p)], ci),
         "gsp_partition_chunk_info": ([p, P(ci), P(ci), P(i64)], ci),
         "gsp_graph_memory": ([p, P(i64), P(i64), P(i64), P(i64)], ci),
+        "gsp_gsddmm_add_leaky": ([p, T, T, ctypes.c_float, T, p], ci),
+        "gsp_gat_forward_additive": ([p, T, T, T, ctypes.c_float, T, T, p], ci),
         "gsp_partition_info": ([p, P(ci), P(ci), P(i64), P(i64), P(i64), P(i64), P(ci)], ci),
         "gsp_status_string": ([ci], ctypes.c_char_p),
         "gsp_last_error_detail": ([], ctypes.c_char_p),
@@ -319,6 +322,30 @@ def _gsddmm_ve(self, X, w, op, side, out=None, stream=None):
     return out
 
 
+def _gsddmm_add_leaky(self, el, er, slope=0.2, out=None, stream=None):
+    """out[j,h] = leaky_relu(el[u_j,h] + er[v,h], slope) -- additive GAT scores (NEXT-3)."""
+    if out is None:
+        out = self._alloc(self.E, el.shape[1], el)
+    de, dr, do = _desc(el), _desc(er), _desc(out)
+    _check(lib.gsp_gsddmm_add_leaky(self._h, ctypes.byref(de), ctypes.byref(dr), float(slope), ctypes.byref(do),
+                                    _stream(stream, el.device)))
+    return out
+
+
+def _gat_forward_additive(self, el, er, Vt, slope=0.2, alpha=None, out=None, stream=None):
+    """alpha = edge_softmax(gsddmm_add_leaky(el, er)); out = gspmm_weighted(Vt, alpha) -- fused."""
+    if alpha is None:
+        alpha = self._alloc(self.E, el.shape[1], el)
+    if out is None:
+        out = self._alloc(self.V, Vt.shape[1], el)
+    de, dr, dv, da, do = _desc(el), _desc(er), _desc(Vt), _desc(alpha), _desc(out)
+    _check(lib.gsp_gat_forward_additive(self._h, ctypes.byref(de), ctypes.byref(dr), ctypes.byref(dv), float(slope),
+                                        ctypes.byref(da), ctypes.byref(do), _stream(stream, el.device)))
+    return alpha, out
+
+
+Graph.gsddmm_add_leaky = _gsddmm_add_leaky
+Graph.gat_forward_additive = _gat_forward_additive
 Graph.gspmm_reduce = _gspmm_reduce
 Graph.gspmm_e = _gspmm_e
 Graph.gsddmm_ve = _gsddmm_ve

@@ -880,3 +880,97 @@ def test_approx_exp_paths_keep_10x_margin(gsp, golden):
     print("approx-exp margins (max err/bound):", worst)
     for k, v in worst.items():
         assert v <= 0.1, f"{k}: max err/bound {v:.3g} > 0.1 (SURVEY L18 10x margin)"
+
+
+# ----------------------------------------- NEXT-3: additive GAT attention
+def _additive_inputs(V, H, Fvh, seed):
+    el = datagen.uniform(seed, V, H, lo=-4, hi=4)
+    er = datagen.uniform(seed + 1, V, H, lo=-4, hi=4)
+    Vh = datagen.uniform(seed + 2, V, H * Fvh)
+    return el, er, Vh
+
+
+@pytest.mark.parametrize("H", [1, 2, 3, 4, 8, 16])
+def test_gsddmm_add_leaky_random(gsp, H):
+    """C14 element by element; T = |el[u]| + |er[v]| (the sum's terms)."""
+    for seed in range(3):
+        rng = np.random.default_rng(40 + seed + H)
+        V = int(rng.integers(1, 3000))
+        E = int(rng.integers(0, 50000))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed != 1
+                    else datagen.skewed_multigraph(V, E, seed, alpha=1.6))
+        G, og = graph_pair(gsp, V, src, dst)
+        el, er, _ = _additive_inputs(V, H, 1, seed)
+        for slope in (0.2, 0.01):
+            ref = og.gsddmm_add_leaky(el, er, slope)
+            rid = np.repeat(np.arange(V), np.diff(og.fwd_off))
+            T = np.abs(el[og.fwd_col]).astype(np.float64) + np.abs(er[rid])
+            out = G.gsddmm_add_leaky(padded(el, H + 3), dev(er), slope)
+            assert_within(out.cpu().numpy(), ref, T, f"add_leaky H{H} s{slope}")
+
+
+def test_gsddmm_add_leaky_t4_golden_and_errors(gsp, golden):
+    g, c = golden("t4.json"), golden("t4_additive.json")
+    G = gsp.Graph(g["V"], g["src"], g["dst"], device=0)
+    el = dev(np.array(c["el"], np.float32)[:, None])
+    er = dev(np.array(c["er"], np.float32)[:, None])
+    out = G.gsddmm_add_leaky(el, er, c["slope"]).cpu().numpy()[:, 0]
+    assert np.allclose(out, c["scores"], rtol=1e-6, atol=1e-7)
+    assert G.gsddmm_add_leaky(el, er, 1.0).cpu().numpy()[:, 0].tolist() == c["scores_slope1"]
+    with pytest.raises(gsp.GspError) as ei:
+        G.gsddmm_add_leaky(el, torch.zeros((4, 2), device="cuda"))
+    assert ei.value.name == "GSP_ERR_SHAPE"
+    with pytest.raises(gsp.GspError) as ei:
+        G.gsddmm_add_leaky(el, er, float("nan"))
+    assert ei.value.name == "GSP_ERR_ARG"
+
+
+def _gat_add_check(gsp, V, src, dst, H, Fvh, seed=0, slope=0.2):
+    G, og = graph_pair(gsp, V, src, dst)
+    el, er, Vh = _additive_inputs(V, H, Fvh, seed)
+    a_ref, o_ref, T = og.gat_forward_additive(el, er, Vh, slope)
+    alpha, out = G.gat_forward_additive(dev(el), dev(er), dev(Vh), slope)
+    ra = assert_within(alpha.cpu().numpy(), a_ref, 1.0, f"add alpha H{H} Fvh{Fvh}")
+    ro = assert_within(out.cpu().numpy(), o_ref, T, f"add out H{H} Fvh{Fvh}")
+    return ra, ro
+
+
+@pytest.mark.parametrize("H,Fvh", [(8, 8), (2, 8), (4, 8), (16, 8), (1, 8), (3, 4), (8, 4)])
+def test_gat_forward_additive_random(gsp, H, Fvh):
+    """C15 (fused one-pass kernel for Fvh = 8, H in {2,4,8,16}; three kernels otherwise)."""
+    for seed in range(2):
+        rng = np.random.default_rng(60 + seed + 7 * H)
+        V = int(rng.integers(2, 2500))
+        E = int(rng.integers(0, 40000))
+        src, dst = (datagen.random_multigraph(V, E, seed) if seed == 0
+                    else datagen.skewed_multigraph(V, E, seed, alpha=1.7))
+        _gat_add_check(gsp, V, src, dst, H, Fvh, seed)
+
+
+def test_gat_forward_additive_heavy_and_boundary_rows(gsp):
+    V, src, dst = _boundary_graph()
+    _gat_add_check(gsp, V, src, dst, 8, 8, seed=3)
+    V, E = 3000, 120_000      # CTA-split hub rows (> 2048 edges), rows past the smem score block
+    src, dst = datagen.skewed_multigraph(V, E, 4, alpha=1.6)
+    _gat_add_check(gsp, V, src, dst, 8, 8, seed=4, slope=0.01)
+    cfg = datagen.CONFIGS["pubmed"]
+    _gat_add_check(gsp, *datagen.make_graph(cfg), cfg.H, cfg.Fh, seed=5)
+
+
+def test_gat_forward_additive_margin(gsp, golden):
+    """SURVEY L18 margin (ex2.approx in the one-pass kernel): <= 0.1 of the bound."""
+    worst = [0.0, 0.0]
+    graphs = [datagen.make_graph("pubmed")]
+    for gf in ("t4.json", "d4.json"):
+        g = golden(gf)
+        graphs.append((g["V"], np.array(g["src"], np.int64), np.array(g["dst"], np.int64)))
+    for seed in range(4):
+        rng = np.random.default_rng(990 + seed)
+        V = int(rng.integers(2, 64)) if seed < 2 else int(rng.integers(200, 3000))
+        graphs.append((V,) + datagen.random_multigraph(V, int(rng.integers(1, 40 * V)), seed))
+    for i, (V, src, dst) in enumerate(graphs):
+        for H in (2, 8):
+            ra, ro = _gat_add_check(gsp, V, src, dst, H, 8, seed=i)
+            worst = [max(worst[0], ra), max(worst[1], ro)]
+    print("additive GAT margins (alpha, out):", worst)
+    assert max(worst) <= 0.1, worst

@@ -20,6 +20,11 @@ if [ -n "$NCU" ]; then
   # the separate chain (gSDDMM, softmax, weighted fwd as their own kernels): 6 after 6
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"spmm|sddmm|softmax" -s 6 -c 6 \
       -o gpurun_out/prof_step_sep python bench.py --profile --chain separate --steps 1 --warmup 1 > gpurun_out/ncu_full_sep.log 2>&1
+  # ogbn-products-shaped gSpMM (DRAM-resident 980 MB table): the timed step's fwd + rev launches
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"spmm" -s 2 -c 2 \
+      -o gpurun_out/prof_products python bench.py --config products --profile --steps 1 --warmup 1 > gpurun_out/ncu_products.log 2>&1
+  [ -f gpurun_out/prof_products.ncu-rep ] && ncu -i gpurun_out/prof_products.ncu-rep --page raw --csv > gpurun_out/prof_products.raw.csv 2>/dev/null
+  rm -f gpurun_out/prof_products.ncu-rep
   # gpurun copies back <= 64 MiB: raw csv of both captures, drop the separate-chain report
   for r in prof_step prof_step_sep; do
     [ -f gpurun_out/$r.ncu-rep ] && ncu -i gpurun_out/$r.ncu-rep --page raw --csv > gpurun_out/$r.raw.csv 2>/dev/null
