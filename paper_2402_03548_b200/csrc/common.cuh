@@ -150,6 +150,15 @@ __device__ __forceinline__ void st_stream_f4(float *p, float4 v, uint64_t pol) {
                  : "memory");
 }
 
+// Packed fp32 pair FMA (FFMA2, sm_100): a[0:2] = w * x[0:2] + a[0:2], each lane
+// an IEEE round-to-nearest fma exactly like FFMA -- half the issue slots of the
+// gather-reduce and dot-product inner loops (DESIGN.md §6 "FFMA2").
+__device__ __forceinline__ void fma2(float &a0, float &a1, float w0, float w1, float x0, float x1) {
+    const float2 r = __ffma2_rn(make_float2(w0, w1), make_float2(x0, x1), make_float2(a0, a1));
+    a0 = r.x;
+    a1 = r.y;
+}
+
 template <int VEC>
 __device__ __forceinline__ void vzero(Vec<VEC> &r) {
 #pragma unroll

@@ -117,12 +117,9 @@ __global__ void __launch_bounds__(kThreads, MINB) gat_fused_kernel(const GatArgs
                     const float x = y[u].v[0] + xv.v[0];
                     sc[u] = x > 0.f ? x : a.slope * x;
                 } else {
-                    float s0 = 0.f, s1 = 0.f;   // two chains: shorter dependency
+                    float s0 = 0.f, s1 = 0.f;   // even / odd features: one FFMA2 per pair
 #pragma unroll
-                    for (int t = 0; t < VEC; t += 2) {
-                        s0 = fmaf(xv.v[t], y[u].v[t], s0);
-                        s1 = fmaf(xv.v[t + 1], y[u].v[t + 1], s1);
-                    }
+                    for (int t = 0; t < VEC; t += 2) fma2(s0, s1, xv.v[t], xv.v[t + 1], y[u].v[t], y[u].v[t + 1]);
                     sc[u] = s0 + s1;
                 }
                 if (FULL || i + u < mcount) {
@@ -153,10 +150,10 @@ __global__ void __launch_bounds__(kThreads, MINB) gat_fused_kernel(const GatArgs
                 St += pu;
                 if constexpr (SAME) {
 #pragma unroll
-                    for (int t = 0; t < VEC; t++) acct.v[t] = fmaf(pu, y[u].v[t], acct.v[t]);
+                    for (int t = 0; t < VEC; t += 2) fma2(acct.v[t], acct.v[t + 1], pu, pu, y[u].v[t], y[u].v[t + 1]);
                 } else {
 #pragma unroll
-                    for (int t = 0; t < VEC; t++) acct.v[t] = fmaf(pu, vv[u].v[t], acct.v[t]);
+                    for (int t = 0; t < VEC; t += 2) fma2(acct.v[t], acct.v[t + 1], pu, pu, vv[u].v[t], vv[u].v[t + 1]);
                 }
             }
         };

@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_PKG, "libgsp.so")
+# GSP_LIB_OVERRIDE: another in-tree build of the same library (A/B timing tools only)
+_SO = os.environ.get("GSP_LIB_OVERRIDE") or os.path.join(_PKG, "libgsp.so")
 
 NORM_NONE, NORM_RIGHT, NORM_BOTH = 0, 1, 2
 REDUCE_SUM, REDUCE_MIN, REDUCE_MAX = 0, 1, 2

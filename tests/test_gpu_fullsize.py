@@ -212,3 +212,27 @@ def test_bench_multi_rank_path_matches_single_gpu(tmp_path):
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 3 and line["multi_gpu_check"]["ok"], line["multi_gpu_check"]
+
+
+@pytest.mark.parametrize("config,ranks,chunks", [("cora", 2, 3), ("arxiv", 2, 0)])
+def test_bench_gcn_multi_rank_paths(config, ranks, chunks):
+    """bench.py's GCN-only step at N > 1 (gloo ranks sharing this GPU): the chunked
+    chunk-major all-gather (Cora, 3 chunks per rank) and the directed graph's
+    reverse as per-source partials + reduce-scatter (ogbn-arxiv-shaped); --check
+    compares every exchanged output per element with the oracle on sampled rows."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GSP_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(ranks),
+           "--master-addr", "127.0.0.1", "--master-port", str(29540 + ranks + chunks), os.path.join(root, "bench.py"),
+           "--gpus", str(ranks), "--config", config, "--steps", "3", "--warmup", "3", "--check", "--no-e2e",
+           "--chunks", str(chunks)]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == ranks and line["multi_gpu_check"]["ok"], line["multi_gpu_check"]
+    if chunks > 1:
+        assert f"{chunks} chunks per rank" in line["config"]["parallelism"]
