@@ -345,7 +345,10 @@ __global__ void __launch_bounds__(kThreads, 2) gat_bwd_kernel(const GatArgs a) {
             for (int u = 0; u < U; u++) {
                 float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-                for (int t = 0; t < VEC; t += 2) fma2(s0, s1, xv.v[t], xv.v[t + 1], y[u].v[t], y[u].v[t + 1]);
+                for (int t = 0; t < VEC; t += 2) {   // (FFMA2 here measured 3 % slower: 4.19 vs 4.05 ms)
+                    s0 = fmaf(xv.v[t], y[u].v[t], s0);
+                    s1 = fmaf(xv.v[t + 1], y[u].v[t + 1], s1);
+                }
                 const float d = s0 + s1;
                 if (i + u < mcount) db[(int64_t)(G * (i + u)) * H] = d;
                 ct = fmaf(av[u], d, ct);

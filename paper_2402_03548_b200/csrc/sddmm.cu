@@ -81,15 +81,8 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
 #pragma unroll
                 for (int q = 0; q < CPL; q++) {
                     float p = 0.f;
-                    if constexpr (VEC >= 2) {   // even / odd features: one FFMA2 per pair
-                        float p1 = 0.f;
 #pragma unroll
-                        for (int t = 0; t < VEC; t += 2)
-                            fma2(p, p1, xv[q].v[t], xv[q].v[t + 1], y[u][q].v[t], y[u][q].v[t + 1]);
-                        p += p1;
-                    } else {
-                        p = fmaf(xv[q].v[0], y[u][q].v[0], p);
-                    }
+                    for (int t = 0; t < VEC; t++) p = fmaf(xv[q].v[t], y[u][q].v[t], p);
 #pragma unroll
                     for (int o = 1; o < CPH; o <<= 1) p += __shfl_xor_sync(kFull, p, o);
                     if (ok && wr[q]) st_stream_f32(ob + (int64_t)(G * (i + u)) * a.ldo + hq[q], p, pol.stream);

@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const SoftmaxBwdA
 #pragma unroll
         for (int k = 0; k < NU; k++)
             if (i0 + 128 * k < hi) {
-                fma2(d[0], d[1], x[k].x, x[k].y, y[k].x, y[k].y);
-                fma2(d[2], d[3], x[k].z, x[k].w, y[k].z, y[k].w);
+                d[0] = fmaf(x[k].x, y[k].x, d[0]); d[1] = fmaf(x[k].y, y[k].y, d[1]);
+                d[2] = fmaf(x[k].z, y[k].z, d[2]); d[3] = fmaf(x[k].w, y[k].w, d[3]);
             }
     }
 #pragma unroll

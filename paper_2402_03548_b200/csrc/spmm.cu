@@ -246,9 +246,11 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
 #pragma unroll
                 for (int q = 0; q < CPL; q++)
 #pragma unroll
-                    for (int t = 0; t < VEC; t += (VEC >= 2 && !MM ? 2 : 1))
+                    for (int t = 0; t < VEC; t += (VEC >= 8 && !MM ? 2 : 1))
                         if constexpr (MM) tile[u % NT][q].v[t] = comb(tile[u % NT][q].v[t], x[u][q].v[t]);
-                        else if constexpr (VEC >= 2)   // FFMA2: two features per instruction
+                        else if constexpr (VEC >= 8)   // FFMA2: two features per instruction (the 256-bit
+                            // path; on the 128-bit DRAM-bound path, e.g. products F = 100, it measured
+                            // 8 % slower: 9.97 vs 9.18 ms same box)
                             fma2(tile[u % NT][q].v[t], tile[u % NT][q].v[t + 1], wt[u][q], wt[u][q], x[u][q].v[t],
                                  x[u][q].v[t + 1]);
                         else tile[u % NT][q].v[t] = fmaf(wt[u][q], x[u][q].v[t], tile[u % NT][q].v[t]);
