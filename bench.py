@@ -538,6 +538,11 @@ def main_gsp(args):
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        elif backend == "fake":
+            # control-flow check of the NCCL path on a 1-GPU box: one process plays rank RANK of
+            # WORLD_SIZE; collectives are shape-checked no-ops (no data moves, no --check)
+            from torch.testing._internal.distributed.fake_pg import FakeStore
+            dist.init_process_group("fake", store=FakeStore(), rank=rank, world_size=world)
         else:
             dist.init_process_group(backend)
     cfg = datagen.CONFIGS[args.config]
@@ -644,7 +649,7 @@ def main_gsp(args):
         else:
             raise KeyError(name)
 
-    overlap = P > 1 and backend == "nccl"
+    overlap = P > 1 and backend in ("nccl", "fake")
     obs = torch.cuda.Stream() if overlap else None
 
     def issue(name, i_out, exch, c, st, pending):
@@ -672,7 +677,7 @@ def main_gsp(args):
                 st["outs"][i_out].copy_(t[rank * R:(rank + 1) * R])
 
     def allreduce_max(v):
-        t = torch.tensor([float(v)], device="cuda" if backend == "nccl" else "cpu")
+        t = torch.tensor([float(v)], device="cuda" if backend in ("nccl", "fake") else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -754,7 +759,7 @@ def main_gsp(args):
 
     # ------------------------------------------- N > 1: check vs the oracle
     check = None
-    if P > 1 and args.check:
+    if P > 1 and args.check and backend != "fake":
         check = multi_gpu_check(args, gsp, torch, dist, rank, P, cfg, kind, V, src, dst, G, parts, new_set,
                                 padded_input, unpad, step, op_defs, s, bq, R, C, allreduce_max)
 
@@ -966,7 +971,9 @@ def main_gsp(args):
                               "what": f"{C} chunk(s) per all-gather; all-gathers / reduce-scatters "
                                       + ("(NCCL, each issued async right after its kernel and overlapped with the "
                                          "next kernels; ms = the residual wait after the last op)"
-                                         if backend == "nccl" else "(host-staged gloo: validation only)")}
+                                         if backend == "nccl" else
+                                         "(fake process group: control-flow check, no data moved)" if backend == "fake"
+                                         else "(host-staged gloo: validation only)")}
 
     # the metric's kernel against its ceilings: the gathered table of Reddit F = 64 is
     # L2-resident, so the bound is the L2 gather rate, measured in this run by the probe

@@ -236,3 +236,27 @@ def test_bench_gcn_multi_rank_paths(config, ranks, chunks):
     assert line["n_gpus"] == ranks and line["multi_gpu_check"]["ok"], line["multi_gpu_check"]
     if chunks > 1:
         assert f"{chunks} chunks per rank" in line["config"]["parallelism"]
+
+
+@pytest.mark.parametrize("config,ranks,rank", [("products", 4, 2), ("reddit", 2, 1), ("arxiv", 2, 0)])
+def test_bench_nccl_path_control_flow(config, ranks, rank):
+    """The NCCL branch of bench.py's N > 1 step on this single GPU: one process plays
+    rank `rank` of `ranks` with torch's fake process group, so the async all-gathers
+    (chunked, chunk-major for products), reduce-scatters, the observer-stream layer
+    timing and the pipelined e2e with collectives all run on CUDA tensors with the
+    NCCL code path's shapes (the fake collectives move no data; parity of the
+    exchanged outputs is the gloo --check tests' job)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GSP_BENCH_BACKEND="fake", WORLD_SIZE=str(ranks), RANK=str(rank), LOCAL_RANK="0")
+    cmd = [sys.executable, os.path.join(root, "bench.py"), "--gpus", str(ranks), "--config", config,
+           "--steps", "3", "--warmup", "3", "--no-configs"]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    if rank == 0:
+        line = json.loads(r.stdout.strip().splitlines()[-1])
+        assert line["n_gpus"] == ranks and line["e2e"]["value"] > 0 and line["value"] > 0
+        assert "fake" in line["per_op"]["exchange"]["what"]

@@ -52,6 +52,27 @@ def run(V, src, dst, F=64, H=8):
         a = pg.gsddmm(Xp, Xp, H=H)
         pg.gspmm_weighted(Xp, a)
         pg.gspmm_weighted(Xp, a, reverse=True)
+    # round 2: additive GAT (one-pass H = 8 and the 3-kernel fallback H = 3), chunked
+    # chunk-major partitions, directed-partition reverse partials, GCN-lean graph
+    el = torch.rand((V, H), device="cuda") - 0.5
+    er = torch.rand((V, H), device="cuda") - 0.5
+    g.gsddmm_add_leaky(el, er, 0.2)
+    g.gat_forward_additive(el, er, X, 0.2)
+    g.gat_forward_additive(el[:, :3].contiguous(), er[:, :3].contiguous(), X3[:, :12].contiguous(), 0.01)
+    C = 3
+    cparts = [g.partition(2, p, device=0, nchunks=C, chunk=c) for p in range(2) for c in range(C)]
+    Xc = torch.zeros((cparts[0].ncols, F), device="cuda")
+    for pg in cparts:
+        pg.gspmm(Xc, 2)
+        pg.gspmm(Xc, 2, reverse=True)
+        pg.gat_forward(Xc, Xc, Xc, H)
+    rs, rd = datagen.rmat(int(np.ceil(np.log2(V))), V, min(10 * V, 30000), 7)   # directed: reverse partials
+    gd = gsp.Graph(V, rs, rd, device=0)
+    for pg in [gd.partition(2, p, device=0) for p in range(2)]:
+        pg.gspmm(torch.zeros((pg.ncols, F), device="cuda"), 2, reverse=True)
+    gl = gsp.Graph(V, src, dst, device=0, edge_ids=False, edge_scales=False)
+    gl.gspmm(X, 2)
+    gl.gspmm(X, 1, reverse=True)
     torch.cuda.synchronize()
 
 V, src, dst = datagen.make_graph("cora")
