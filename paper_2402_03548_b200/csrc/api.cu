@@ -472,6 +472,7 @@ gsp_status gsp_gspmm(const gsp_graph *g, const gsp_tensor *X, int norm, gsp_tens
     a.F = X->cols;
     a.row_scale = S.row_scale[norm]; a.col_scale = S.col_scale[norm]; a.edge_scale = S.edge_scale[norm];
     a.H = 1; a.Fh = X->cols > 0 ? X->cols : 1;
+    a.light = S.nnz < 32 * S.nrows;
     cudaError_t e = gsp::launch_spmm(a, gsp::kSpmmScaled, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "gspmm launch");
     return GSP_OK;

@@ -27,6 +27,7 @@ struct SpmmArgs {
     int64_t H, Fh;
     int pf;                  // L2 prefetch distance of the edge streams, in 32-edge tiles (0 = off)
     int wpol;                // L2 policy of the weight rows: 0 evict_first (streamed once), 1 evict_normal, 2 evict_last
+    int light;               // mean degree < 32 (set by the caller): launch shapes that favour rows in flight
     int out_vec;             // out rows 16-B aligned (ldo % 4 == 0): vector stores, else scalar (set by launch_spmm)
 };
 

@@ -533,6 +533,13 @@ cudaError_t spmm_go(const SpmmArgs &a, int mode, int64_t slabs, cudaStream_t s) 
             default: break;
         }
     }
+    if constexpr (VEC == 8 && LPE == 16 && CPL == 1) {   // F = 65-128 with 32-B rows (ogbn-arxiv F = 128)
+        // light graphs (mean degree < 32): a row is a few 2-edge gather instructions, so the
+        // launch is bound by rows in flight x per-row latency -- 2 gathers in flight per lane
+        // at 4 CTAs/SM (more warps) beat 4 at 3: arxiv 127 -> 103 us (same-box A/B; 2 at 6
+        // CTAs/SM 205, 4 at 4 137, 8 at 2 164 us)
+        if (mode == kSpmmScaled && a.light) return spmm_go_v<VEC, LPE, CPL, 2, 4>(a, mode, slabs, s);
+    }
     if constexpr (VEC == 4 && LPE == 32 && CPL == 1) {   // rows of 17-32 float4 chunks (e.g. F = 100)
         // scaled gSpMM on a DRAM-resident table (ogbn-products F = 100): 8 gathers in flight
         // per lane at 3 CTAs/SM, 9.92 -> 9.18 ms (2 CTAs/SM: 10.6; U = 16: 10.3)
