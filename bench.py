@@ -915,6 +915,11 @@ def main_gsp(args):
         ms_sbw = time_op(lambda: G.edge_softmax_backward(s, dal, out=dal, stream=stream))
         ms_gbw = time_op(lambda: G.gat_backward_scores(dO, Z, s, out=alpha2, stream=stream))
         ms_gbw_sep = time_op(lambda: G.gsddmm(dO, Z, out=alpha2, stream=stream)) + ms_sbw
+        # NEXT-3 additive GAT attention: scores alone and the fused forward (alpha + aggregate)
+        el = Z[:, :H].contiguous()
+        er = dO[:, :H].contiguous()
+        ms_add = time_op(lambda: G.gsddmm_add_leaky(el, er, 0.2, out=alpha2, stream=stream))
+        ms_gat_add = time_op(lambda: G.gat_forward_additive(el, er, Z, 0.2, alpha=alpha2, out=gout, stream=stream))
         sep = sum((outside if fused else avg)[k] for k in ("gsddmm", "edge_softmax", "gspmm_weighted_fwd"))
         next_rows = {
             "gat_forward_fused": {"row": "NEXT-2", "ms": round(ms_gat, 4), "in_step": fused,
@@ -927,13 +932,21 @@ def main_gsp(args):
             "gsddmm_ve_add_src": {"row": "NEXT-3", "ms": round(ms_ve, 4),
                                   "GB_s": round((2 * Eloc * H * 4 + Eloc * 4 + (Vloc + 1) * 8 + V * H * 4)
                                                 / (ms_ve * 1e-3) / 1e9, 1)},
+            "gsddmm_add_leaky": {"row": "NEXT-3", "ms": round(ms_add, 4),
+                                 "GB_s": round((Eloc * 4 + Eloc * H * 4 + Eloc * H * 4 + (Vloc + 1) * 8 + V * H * 4)
+                                               / (ms_add * 1e-3) / 1e9, 1),
+                                 "what": "additive GAT scores lrelu(el[u] + er[v]), H = 8"},
+            "gat_forward_additive_fused": {"row": "NEXT-3", "ms": round(ms_gat_add, 4),
+                                           "GE_s": round(Eloc / (ms_gat_add * 1e-3) / 1e9, 3),
+                                           "what": "alpha = softmax(lrelu(el[u] + er[v])), out = sum alpha Z[u], "
+                                                   "one pass, alpha written (H = 8, Fh = 8)"},
             "gat_backward_scores_fused": {"row": "NEXT-1", "ms": round(ms_gbw, 4),
                                           "vs_gsddmm_plus_softmax_backward_ms": round(ms_gbw_sep, 4)},
             "edge_softmax_backward": {"row": "NEXT-1", "ms": round(ms_sbw, 4),
                                       "GB_s": round(alg_bytes("edge_softmax", Vloc, Eloc, F, H) * 1.5
                                                     / (ms_sbw * 1e-3) / 1e9, 1)},
         }
-        del alpha2, gout, dal, hout_
+        del alpha2, gout, dal, hout_, el, er
         # context: warm-L2 time of the headline op (no flush: steady
         # state layer to layer) and the paper's kernel-plot shapes (F = 32, one head:
         # P:2308) on the same graph

@@ -25,6 +25,15 @@ if [ -n "$NCU" ]; then
       -o gpurun_out/prof_products python bench.py --config products --profile --steps 1 --warmup 1 > gpurun_out/ncu_products.log 2>&1
   [ -f gpurun_out/prof_products.ncu-rep ] && ncu -i gpurun_out/prof_products.ncu-rep --page raw --csv > gpurun_out/prof_products.raw.csv 2>/dev/null
   rm -f gpurun_out/prof_products.ncu-rep
+  # Reddit F = 602 (561 MB table, ld 604) and ogbn-arxiv F = 128: one gSpMM fwd launch each, after opbench's 3 warm-ups
+  timeout 600 ncu --set full --clock-control none -k regex:"spmm" -s 3 -c 1 -o gpurun_out/prof_f602 \
+      python tools/opbench.py --F 602 --ld 604 --ops gspmm_fwd --reps 1 > gpurun_out/ncu_f602.log 2>&1
+  timeout 600 ncu --set full --clock-control none -k regex:"spmm" -s 3 -c 1 -o gpurun_out/prof_arxiv \
+      python tools/opbench.py --config arxiv --ops gspmm_fwd --reps 1 > gpurun_out/ncu_arxiv.log 2>&1
+  for r in prof_f602 prof_arxiv; do
+    [ -f gpurun_out/$r.ncu-rep ] && ncu -i gpurun_out/$r.ncu-rep --page raw --csv > gpurun_out/$r.raw.csv 2>/dev/null
+    rm -f gpurun_out/$r.ncu-rep
+  done
   # gpurun copies back <= 64 MiB: raw csv of both captures, drop the separate-chain report
   for r in prof_step prof_step_sep; do
     [ -f gpurun_out/$r.ncu-rep ] && ncu -i gpurun_out/$r.ncu-rep --page raw --csv > gpurun_out/$r.raw.csv 2>/dev/null
