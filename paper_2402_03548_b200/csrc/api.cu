@@ -620,6 +620,7 @@ gsp_status gsp_gat_forward(const gsp_graph *g, const gsp_tensor *X, const gsp_te
     gsp::GatArgs ga{};
     ga.off = S.off; ga.col = S.col; ga.order = S.order; ga.task = S.task; ga.nrows = S.nrows; ga.n_heavy = S.n_heavy;
     ga.row_base = g->row_base;
+    ga.light = S.nnz < 32 * S.nrows;
     ga.X = static_cast<const float *>(X->data); ga.ldx = X->ld;
     ga.Y = static_cast<const float *>(Y->data); ga.ldy = Y->ld;
     ga.Vt = static_cast<const float *>(Vt->data); ga.ldv = Vt->ld;
@@ -679,6 +680,7 @@ gsp_status gsp_gat_backward_scores(const gsp_graph *g, const gsp_tensor *dOut, c
     gsp::GatArgs ga{};
     ga.off = S.off; ga.col = S.col; ga.order = S.order; ga.task = S.task; ga.nrows = S.nrows; ga.n_heavy = S.n_heavy;
     ga.row_base = g->row_base;
+    ga.light = S.nnz < 32 * S.nrows;
     ga.X = static_cast<const float *>(dOut->data); ga.ldx = dOut->ld;
     ga.Y = ga.X; ga.ldy = dOut->ld;
     ga.Vt = static_cast<const float *>(Vt->data); ga.ldv = Vt->ld;
@@ -775,6 +777,7 @@ gsp_status gsp_gat_forward_additive(const gsp_graph *g, const gsp_tensor *el, co
     gsp::GatArgs ga{};
     ga.off = S.off; ga.col = S.col; ga.order = S.order; ga.task = S.task; ga.nrows = S.nrows; ga.n_heavy = S.n_heavy;
     ga.row_base = g->row_base;
+    ga.light = S.nnz < 32 * S.nrows;
     ga.X = static_cast<const float *>(er->data); ga.ldx = er->ld;
     ga.Y = static_cast<const float *>(el->data); ga.ldy = el->ld;
     ga.Vt = static_cast<const float *>(Vt->data); ga.ldv = Vt->ld;

@@ -459,8 +459,8 @@ AttrFlags &gat_bwd_attr() {
 }
 
 template <int HH, int MODE, int UO = 0, int MB = 2>
-cudaError_t launch_gat_v(GatArgs a, dim3 grid, cudaStream_t s) {
-    a.sc_cap = (gat_score_bytes() / (4 * HH)) & ~int64_t(31);   // whole 32-edge tiles
+cudaError_t launch_gat_v(GatArgs a, dim3 grid, cudaStream_t s, int64_t score_bytes = -1) {
+    a.sc_cap = ((score_bytes >= 0 ? score_bytes : gat_score_bytes()) / (4 * HH)) & ~int64_t(31);   // whole 32-edge tiles
     const size_t dyn = (size_t)(kWarps * a.sc_cap * HH * 4);
     cudaError_t e = opt_in_smem(gat_fused_kernel<HH, MODE, UO, MB>, dyn, gat_fused_attr<HH, MODE, UO, MB>());
     if (e != cudaSuccess) return e;
@@ -480,6 +480,11 @@ static int tune_gat() {
 template <int HH, int MODE>
 cudaError_t launch_gat_h(GatArgs a, dim3 grid, cudaStream_t s) {
     if constexpr (HH == 8) {
+        // light graphs (mean degree < 32, e.g. Pubmed): rows are one or two tiles, so rows in
+        // flight decide -- 2 edges in flight per lane at 4 CTAs/SM with a 2 KB score block
+        // (64 edges per warp): Pubmed 8 x 8 34.8 -> 26.6 us (same-box A/B; 4 at 3 CTAs/SM with
+        // 3 KB 28.7 us)
+        if (a.light && tune_gat() == 0) return launch_gat_v<HH, MODE, 2, 4>(a, grid, s, 2048);
         switch (tune_gat()) {
             case 1: return launch_gat_v<HH, MODE, 4, 3>(a, grid, s);
             case 2: return launch_gat_v<HH, MODE, 4, 2>(a, grid, s);

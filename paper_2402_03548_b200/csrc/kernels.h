@@ -101,6 +101,7 @@ struct GatArgs {
     int64_t ldo;
     int64_t H;
     int64_t sc_cap;    // edges per warp slice whose raw scores stay in shared memory (set by the launcher)
+    int light;         // mean degree < 32 (set by the caller): launch shape favouring rows in flight
     int additive;      // 0: scores <X[v], Y[u]> (Fh = 8); 1: lrelu(Y[u,h] + X[v,h], slope) (X = er, Y = el: [ncols, H])
     float slope;
 };
