@@ -122,6 +122,66 @@ def test_reddit_gat_forward_fused_sampled(reddit):
     within(out[torch.from_numpy(rows).cuda()].cpu().numpy(), o_ref[rows], T[rows])
 
 
+def test_reddit_gat_forward_additive_sampled(reddit):
+    """NEXT-3 at full size: the fused additive GAT forward (alpha = softmax(lrelu(el[u]
+    + er[v])), aggregate of Z, H = 8 x 8) on sampled rows against oracle C15 on the
+    sub-graph of those rows' in-edges."""
+    cfg, G, og = reddit
+    H, F = cfg.H, cfg.H * cfg.Fh
+    rows = sample_rows(og.fwd_off, 95)
+    eids = og.row_edges(rows)
+    sub = oracle.Graph(og.V, og.fwd_col[eids].astype(np.int64),
+                       np.repeat(rows, og.fwd_off[rows + 1] - og.fwd_off[rows]))
+    elh = datagen.uniform(31, og.V, H, lo=-4, hi=4)
+    erh = datagen.uniform(32, og.V, H, lo=-4, hi=4)
+    Zh = datagen.uniform(33, og.V, F)
+    alpha, out = G.gat_forward_additive(dev(elh), dev(erh), dev(Zh), 0.2)
+    a_ref, o_ref, T = sub.gat_forward_additive(elh, erh, Zh, 0.2)
+    within(alpha[torch.from_numpy(eids).cuda()].cpu().numpy(), a_ref, 1.0)
+    within(out[torch.from_numpy(rows).cuda()].cpu().numpy(), o_ref[rows], T[rows])
+
+
+def test_products_chunked_partitions_bench_layout():
+    """ogbn-products in bench.py's N = 8 launch configuration: 8 ranks x 4 chunks of
+    chunk-major partitions, run one after another on this GPU, each writing its
+    [R, F] block into its chunk's all-gather range of the padded table (the NCCL
+    all-gather replaced by the placement).  Un-padded rows, sampled (heaviest,
+    random, lightest), against oracle C4 from the COO list; forward and the
+    symmetric reverse."""
+    import paper_2402_03548_b200 as gsp
+    cfg = datagen.CONFIGS["products"]
+    V, src, dst = datagen.make_graph(cfg)
+    G = gsp.Graph(V, src, dst, device=0)
+    P, C = 8, 4
+    b = G.partition_bounds(P * C)
+    slot = lambda q: (q % C) * P + q // C
+    Xh = datagen.uniform(0x960D + 1, V, cfg.F)
+    R = None
+    tables = {}
+    for p in range(P):
+        for c in range(C):
+            pg = G.partition(P, p, device=0, nchunks=C, chunk=c)
+            if R is None:
+                R = pg.R
+                Xp = torch.zeros((pg.ncols, cfg.F), device="cuda")
+                for q in range(P * C):
+                    Xp[slot(q) * R:slot(q) * R + b[q + 1] - b[q]] = dev(Xh[b[q]:b[q + 1]])
+                for r in (False, True):
+                    tables[r] = torch.full((pg.ncols, cfg.F), float("nan"), device="cuda")
+            for rev in (False, True):
+                pg.gspmm(Xp, gsp.NORM_BOTH, out=tables[rev][(c * P + p) * R:(c * P + p + 1) * R], reverse=rev)
+            torch.cuda.synchronize()
+            del pg
+    off = G.export(rev=False, coo=False)["fwd_off"]
+    rows = sample_rows(off, 5)
+    q_of = np.searchsorted(b, rows, side="right") - 1
+    pos = torch.from_numpy(np.array([slot(q) * R + r - b[q] for q, r in zip(q_of, rows)])).cuda()
+    for rev in (False, True):
+        got = tables[rev][pos].cpu().numpy()
+        ref, T = oracle.gspmm_rows_coo(V, src, dst, Xh, 2, rows, reverse=rev, F=cfg.F)
+        within(got, ref, T)
+
+
 def test_reddit_gat_backward_scores_sampled(reddit):
     """The fused GAT backward scores (NEXT-1) at full size, as bench.py's next_rows
     calls it (dOut, Z, alpha of the forward, H = 8 x 8): ds of sampled rows against

@@ -37,6 +37,8 @@ s = torch.empty((E, H), device="cuda")
 s2 = torch.rand((E, H), device="cuda")
 outh = torch.empty((V, H), device="cuda")
 flush = torch.empty(512 << 18, device="cuda")
+el = Z[:, :H].contiguous()
+er = Z[:, H:2 * H].contiguous()
 ops = {
     "gspmm_fwd": lambda: G.gspmm(X, 2, out=out),
     "gspmm_rev": lambda: G.gspmm(X, 2, out=out, reverse=True),
@@ -48,6 +50,8 @@ ops = {
     "wfwd": lambda: G.gspmm_weighted(Z, s, out=outg),
     "wrev": lambda: G.gspmm_weighted(Z, s, out=outg, reverse=True),
     "gat_fused": lambda: G.gat_forward(Z, Z, Z, H, alpha=s, out=outg),
+    "gat_add": lambda: G.gat_forward_additive(el, er, Z, 0.2, alpha=s, out=outg),
+    "add_leaky": lambda: G.gsddmm_add_leaky(el, er, 0.2, out=s),
     "gat_bwd": lambda: G.gat_backward_scores(Z, Z, s, out=s2),
     "softmax_bwd": lambda: G.edge_softmax_backward(s, s2, out=s2),
     "e_sum": lambda: G.gspmm_e(s, 0, out=outh),
