@@ -562,70 +562,89 @@ def main_gsp(args):
     stream = torch.cuda.current_stream()
 
     P = world
-    C = 1
-    if P > 1:
-        C = args.chunks or (4 if args.config == "products" else 1)
-        if not G.symmetric or kind == "gat":
-            C = 1      # per-source partials (reduce-scatter) need one block per rank
-        parts = [G.partition(P, rank, device=local, nchunks=C, chunk=c) for c in range(C)]
-        R = parts[0].R
-        bq = G.partition_bounds(P * C)
-        slot = lambda q: (q % C) * P + q // C
-    else:
-        parts = [G]
-        R = V
-        bq = np.array([0, V])
-        slot = lambda q: 0
-    ncols = parts[0].ncols
-    Q = P * C
 
-    def padded_input(seed):
-        Xh = datagen.uniform(seed, V, F)
-        if P == 1:
-            return torch.from_numpy(Xh).cuda()
-        Xp = torch.zeros((ncols, F), device="cuda")
-        for q in range(Q):
-            Xp[slot(q) * R:slot(q) * R + bq[q + 1] - bq[q]] = torch.from_numpy(Xh[bq[q]:bq[q + 1]]).cuda()
-        return Xp
+    class Layout:
+        """one padded table layout of the N > 1 step: this rank's C chunk
+        partitions (chunk-major slots; C = 1 is the plain rank-major layout)"""
 
-    def unpad(t):
-        if P == 1:
-            return t
-        return torch.cat([t[slot(q) * R:slot(q) * R + bq[q + 1] - bq[q]] for q in range(Q)])
+        def __init__(self, C):
+            self.C = C
+            if P > 1:
+                self.parts = [G.partition(P, rank, device=local, nchunks=C, chunk=c) for c in range(C)]
+                self.R = self.parts[0].R
+                self.bq = G.partition_bounds(P * C)
+            else:
+                self.parts, self.R, self.bq = [G], V, np.array([0, V])
+            self.ncols = self.parts[0].ncols
+            self.E = sum(pg.E for pg in self.parts)
+            self.lo, self.hi = int(self.bq[rank * C]), int(self.bq[(rank + 1) * C])   # this rank's rows
 
-    ins0 = tuple(padded_input(cfg.seed + k) for k in range(4 if kind == "gat" else 2))
-    Eloc = sum(pg.E for pg in parts)
+        def slot(self, q):
+            return (q % self.C) * P + q // self.C
+
+        def padded(self, Xh):
+            if P == 1:
+                return torch.from_numpy(Xh).cuda()
+            Xp = torch.zeros((self.ncols, F), device="cuda")
+            for q in range(P * self.C):
+                s0 = self.slot(q) * self.R
+                Xp[s0:s0 + self.bq[q + 1] - self.bq[q]] = torch.from_numpy(Xh[self.bq[q]:self.bq[q + 1]]).cuda()
+            return Xp
+
+        def unpad(self, t):
+            if P == 1:
+                return t
+            return torch.cat([t[self.slot(q) * self.R:self.slot(q) * self.R + self.bq[q + 1] - self.bq[q]]
+                              for q in range(P * self.C)])
+
+    # GCN ops: chunked all-gathers on symmetric graphs (each chunk's all-gather overlaps the
+    # next chunk's kernel); a directed graph's reverse and the GAT ops (alpha, per-source
+    # partials + reduce-scatter) use the unchunked layout.  The all-gather moves the whole
+    # [V, F] table while the kernel moves ~E rows, so it only matters next to the compute on
+    # low-degree graphs (ogbn-products, mean 50: 0.95 ms vs 1.3 ms at P = 8, SURVEY §8(e));
+    # on Reddit (mean 492: ~60 us vs 0.2 ms) chunks would only add launches
+    # (tools/part_cost.py: P = 8 rank compute 0.22 / 0.23 / 0.32 ms at C = 1 / 2 / 4)
+    Cg = 1
+    if P > 1 and G.symmetric:
+        Cg = args.chunks or (4 if G.E < 128 * V else 1)
+    lay_gcn = Layout(Cg)
+    lay_one = lay_gcn if Cg == 1 else Layout(1)
     fused = args.chain == "fused"
-    # output buffers of one step: out [C*R, F] per vertex output (chunk c = rows c*R..),
-    # partial [ncols, F] for per-source partial ops, gathered [ncols, F] for all-gathered ones
     rev_partial = P > 1 and not G.symmetric                     # directed GCN backward at N > 1
+    # op: (name, input index, output index, exchange, layout)
     if kind == "gcn":
-        op_defs = [("gspmm_fwd", 0, 0, "ag"), ("gspmm_rev", 1, 1, "rs" if rev_partial else "ag")]
+        op_defs = [("gspmm_fwd", 0, 0, "ag", lay_gcn),
+                   ("gspmm_rev", 1, 1, "rs", lay_one) if rev_partial else ("gspmm_rev", 1, 1, "ag", lay_gcn)]
     else:
-        op_defs = [("gspmm_fwd", 0, 0, "ag"), ("gspmm_rev", 1, 1, "ag")]
+        op_defs = [("gspmm_fwd", 0, 0, "ag", lay_gcn), ("gspmm_rev", 1, 1, "ag", lay_gcn)]
         if fused:
-            op_defs.append(("gat_forward", 2, 2, "ag"))
+            op_defs.append(("gat_forward", 2, 2, "ag", lay_one))
         else:
-            op_defs += [("gsddmm", 2, None, None), ("edge_softmax", None, None, None),
-                        ("gspmm_weighted_fwd", None, 2, "ag")]
-        op_defs.append(("gspmm_weighted_rev", 3, 3, "rs"))
+            op_defs += [("gsddmm", 2, None, None, lay_one), ("edge_softmax", None, None, None, lay_one),
+                        ("gspmm_weighted_fwd", None, 2, "ag", lay_one)]
+        op_defs.append(("gspmm_weighted_rev", 3, 3, "rs", lay_one))
     op_names = [d[0] for d in op_defs]
     nout = 1 + max(d[2] for d in op_defs if d[2] is not None)
+    in_lay = {d[1]: d[4] for d in op_defs if d[1] is not None}     # the layout of each input table
+    out_lay = {d[2]: d[4] for d in op_defs if d[2] is not None}
+    ins0 = tuple(in_lay[k].padded(datagen.uniform(cfg.seed + k, V, F)) for k in range(4 if kind == "gat" else 2))
+    Eloc = lay_one.E                                     # this rank's edges (alpha rows)
+    R, ncols = lay_one.R, lay_one.ncols                  # per-op figures below use the unchunked layout
     s = torch.empty((Eloc, H), device="cuda") if kind == "gat" else None
 
     def new_set(ins):
-        outs = [torch.empty((C * R if P > 1 else V, F), device="cuda") for _ in range(nout)]
-        partial = {d[2]: torch.empty((ncols, F), device="cuda") for d in op_defs if d[3] == "rs" and P > 1}
-        gathered = {d[2]: torch.empty((ncols, F), device="cuda") for d in op_defs if d[3] == "ag" and P > 1}
+        outs = [torch.empty((out_lay[i].C * out_lay[i].R if P > 1 else V, F), device="cuda") for i in range(nout)]
+        partial = {d[2]: torch.empty((d[4].ncols, F), device="cuda") for d in op_defs if d[3] == "rs" and P > 1}
+        gathered = {d[2]: torch.empty((d[4].ncols, F), device="cuda") for d in op_defs if d[3] == "ag" and P > 1}
         return {"ins": ins, "outs": outs, "partial": partial, "gathered": gathered}
 
     set0 = new_set(ins0)
 
-    def launch(name, c, st):
-        """kernel of op `name` for chunk c with the buffers of set st"""
-        pg = parts[c]
+    def launch(name, c, st, L):
+        """kernel of op `name` for chunk c of layout L with the buffers of set st"""
+        pg = L.parts[c]
         ins, outs = st["ins"], st["outs"]
-        o = (lambda i: outs[i][c * R:(c + 1) * R]) if P > 1 else (lambda i: outs[i])
+        o = (lambda i: outs[i][c * L.R:(c + 1) * L.R]) if P > 1 else (lambda i: outs[i])
         if name == "gspmm_fwd":
             pg.gspmm(ins[0], gsp.NORM_BOTH, out=o(0), stream=stream)
         elif name == "gspmm_rev":
@@ -652,29 +671,29 @@ def main_gsp(args):
     overlap = P > 1 and backend in ("nccl", "fake")
     obs = torch.cuda.Stream() if overlap else None
 
-    def issue(name, i_out, exch, c, st, pending):
+    def issue(name, i_out, exch, c, st, pending, L):
         """NCCL: the op's collective for chunk c, issued async right after its kernel"""
         if not overlap or exch is None:
             return
         if exch == "ag":
-            w = dist.all_gather_into_tensor(st["gathered"][i_out][c * P * R:(c + 1) * P * R],
-                                            st["outs"][i_out][c * R:(c + 1) * R], async_op=True)
+            w = dist.all_gather_into_tensor(st["gathered"][i_out][c * P * L.R:(c + 1) * P * L.R],
+                                            st["outs"][i_out][c * L.R:(c + 1) * L.R], async_op=True)
         else:
             w = dist.reduce_scatter_tensor(st["outs"][i_out], st["partial"][i_out], async_op=True)
         pending.setdefault(name, []).append(w)
 
     def host_exchange(st):
         """gloo (validation on a 1-GPU box): host-staged equivalent after the step"""
-        for name, _, i_out, exch in op_defs:
+        for name, _, i_out, exch, L in op_defs:
             if exch == "ag":
-                for c in range(C):
-                    blk = [torch.empty((R, F)) for _ in range(P)]
-                    dist.all_gather(blk, st["outs"][i_out][c * R:(c + 1) * R].cpu())
-                    st["gathered"][i_out][c * P * R:(c + 1) * P * R].copy_(torch.cat(blk))
+                for c in range(L.C):
+                    blk = [torch.empty((L.R, F)) for _ in range(P)]
+                    dist.all_gather(blk, st["outs"][i_out][c * L.R:(c + 1) * L.R].cpu())
+                    st["gathered"][i_out][c * P * L.R:(c + 1) * P * L.R].copy_(torch.cat(blk))
             elif exch == "rs":
                 t = st["partial"][i_out].cpu()
                 dist.all_reduce(t)
-                st["outs"][i_out].copy_(t[rank * R:(rank + 1) * R])
+                st["outs"][i_out].copy_(t[rank * L.R:(rank + 1) * L.R])
 
     def allreduce_max(v):
         t = torch.tensor([float(v)], device="cuda" if backend in ("nccl", "fake") else "cpu")
@@ -691,10 +710,10 @@ def main_gsp(args):
         marks = [mark()] if record else None
         pending = {}
         layer = None
-        for name, _, i_out, exch in op_defs:
-            for c in range(C):
-                launch(name, c, st)
-                issue(name, i_out, exch, c, st, pending)
+        for name, _, i_out, exch, L in op_defs:
+            for c in range(L.C):
+                launch(name, c, st, L)
+                issue(name, i_out, exch, c, st, pending, L)
             if record:
                 marks.append(mark())
             if record and name == "gspmm_fwd":
@@ -760,8 +779,8 @@ def main_gsp(args):
     # ------------------------------------------- N > 1: check vs the oracle
     check = None
     if P > 1 and args.check and backend != "fake":
-        check = multi_gpu_check(args, gsp, torch, dist, rank, P, cfg, kind, V, src, dst, G, parts, new_set,
-                                padded_input, unpad, step, op_defs, s, bq, R, C, allreduce_max)
+        check = multi_gpu_check(args, gsp, torch, dist, rank, P, cfg, kind, V, src, dst, G, new_set, in_lay,
+                                step, op_defs, allreduce_max)
 
     # ---------------------------------------------------------------- e2e
     # The same step through the C ABI with HOST buffers: every step copies its input
@@ -774,7 +793,7 @@ def main_gsp(args):
     e2e = None
     if not args.no_e2e and not args.profile and (P == 1 or overlap):
         nin = len(ins0)
-        hin = [torch.empty((ncols, F), dtype=torch.float32).pin_memory() for _ in range(nin)]
+        hin = [torch.empty(tuple(t.shape), dtype=torch.float32).pin_memory() for t in ins0]
         for h, d in zip(hin, ins0):
             h.copy_(d.cpu())
         sets = [set0, new_set(tuple(torch.empty_like(t) for t in ins0))]
@@ -805,12 +824,12 @@ def main_gsp(args):
                 if out_free[j] is not None:         # step k-2's outputs have left this set
                     stream.wait_event(out_free[j])
                 done, pending = [], {}
-                for name, i_in, i_out, exch in defs:
+                for name, i_in, i_out, exch, L in defs:
                     if i_in is not None:
                         stream.wait_event(ready[i_in])
-                    for c in range(C):
-                        launch(name, c, st)
-                        issue(name, i_out, exch, c, st, pending)
+                    for c in range(L.C):
+                        launch(name, c, st, L)
+                        issue(name, i_out, exch, c, st, pending, L)
                     if i_out is not None and P == 1:
                         e = torch.cuda.Event()
                         e.record(stream)
@@ -981,7 +1000,7 @@ def main_gsp(args):
                      "reuse": round(bytes_of[k] / traffic[k], 2) if traffic.get(k) else None}
     if P > 1:
         per_op["exchange"] = {"ms": round(avg["exchange"], 4),
-                              "what": f"{C} chunk(s) per all-gather; all-gathers / reduce-scatters "
+                              "what": f"GCN ops {Cg} chunk(s) per all-gather; all-gathers / reduce-scatters "
                                       + ("(NCCL, each issued async right after its kernel and overlapped with the "
                                          "next kernels; ms = the residual wait after the last op)"
                                          if backend == "nccl" else
@@ -1060,7 +1079,7 @@ def main_gsp(args):
                                 (src, dst) if oracle_ok else None)
 
     if rank == 0:
-        launches = len(op_names) * C * args.steps
+        launches = sum(d[4].C for d in op_defs) * args.steps
         line = {
             "metric": METRIC,
             "value": round(value, 4), "unit": "GE/s",
@@ -1079,8 +1098,8 @@ def main_gsp(args):
                        "V": V, "E": E, "F": F, "H": H or None, "Fh": cfg.Fh or None,
                        "graph": f"Chung-Lu beta={cfg.beta}, seed={cfg.seed:#x}" if cfg.kind == "chung_lu"
                        else f"R-MAT scale {cfg.scale}, seed={cfg.seed:#x}",
-                       "parallelism": (f"row-partition x{P}" + (f", {C} chunks per rank" if C > 1 else ""))
-                       if P > 1 else "single GPU",
+                       "parallelism": (f"row-partition x{P}" + (f", {Cg} chunks per rank for the GCN ops"
+                                                                 if Cg > 1 else "")) if P > 1 else "single GPU",
                        "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",
                        "edge_visits_per_step": visits},
             "step": {"ops": op_names, "ms": round(t_step, 4), "GE_s": round(visits / (t_step * 1e-3) / 1e9, 4),
@@ -1107,34 +1126,36 @@ def main_gsp(args):
         dist.destroy_process_group()
 
 
-def multi_gpu_check(args, gsp, torch, dist, rank, P, cfg, kind, V, src, dst, G, parts, new_set, padded_input,
-                    unpad, step, op_defs, s, bq, R, C, allreduce_max):
+def multi_gpu_check(args, gsp, torch, dist, rank, P, cfg, kind, V, src, dst, G, new_set, in_lay, step, op_defs,
+                    allreduce_max):
     """N > 1 --check: one step on seeded inputs, then every exchanged output of
     sampled rows against the oracle per element (north_star bound).  The GAT
     weighted reverse gets seeded weights w (the oracle's C5 input) instead of alpha;
     each rank holds w for its own edge-id range."""
     import oracle
     F, H = cfg.F, cfg.H
-    st = new_set(tuple(padded_input(cfg.seed + 100 + k) for k in range(4 if kind == "gat" else 2)))
+    nin = 4 if kind == "gat" else 2
+    Xh = [datagen.uniform(cfg.seed + 100 + k, V, F) for k in range(nin)]
+    st = new_set(tuple(in_lay[k].padded(Xh[k]) for k in range(nin)))
     step(False, st)
     torch.cuda.synchronize()
-    Xh = [datagen.uniform(cfg.seed + 100 + k, V, F) for k in range(4 if kind == "gat" else 2)]
     res = {}
     ex = G.export(rev=True, coo=False)
-    fin = {}
-    for name, _, i_out, exch in op_defs:
+    fin, lay = {}, {}
+    for name, _, i_out, exch, L in op_defs:
         if i_out is None:
             continue
+        lay[name] = L
         if exch == "ag":
-            fin[name] = unpad(st["gathered"][i_out]).cpu().numpy()
-        else:   # rs: this rank's own rows of the slot-major layout
+            fin[name] = L.unpad(st["gathered"][i_out]).cpu().numpy()
+        else:   # rs: this rank's own rows of the rank-major layout
             fin[name] = st["outs"][i_out].cpu().numpy()
-    lo, hi = int(bq[rank * C]), int(bq[(rank + 1) * C])
     for name, off, rev in (("gspmm_fwd", ex["fwd_off"], False), ("gspmm_rev", ex["rev_off"], True)):
         rows = sample_rows(off, 7 + int(rev))
         ref, T = oracle.gspmm_rows_coo(V, src, dst, Xh[int(rev)], 2, rows, reverse=rev, F=F)
         got = fin[name]
         if got.shape[0] != V:            # reduce-scatter output: only this rank's rows
+            lo, hi = lay[name].lo, lay[name].hi
             rows_m = rows[(rows >= lo) & (rows < hi)]
             sel = np.isin(rows, rows_m)
             got, ref, T, rows = got[rows_m - lo], ref[sel], T[sel], rows_m
@@ -1150,14 +1171,16 @@ def multi_gpu_check(args, gsp, torch, dist, rank, P, cfg, kind, V, src, dst, G, 
         res["gat_forward"] = ratio(fin.get("gat_forward", fin.get("gspmm_weighted_fwd"))[rows], o_ref[rows],
                                    oracle.bound(T[rows]))
         # weighted reverse with seeded weights: this rank's w rows = its edge-id range
+        L = lay["gspmm_weighted_rev"]
+        lo, hi = L.lo, L.hi
         wh = datagen.uniform(cfg.seed + 200, og.E, H, lo=0, hi=1)
         e0, e1 = og.fwd_off[lo], og.fwd_off[hi]
         wloc = torch.from_numpy(wh[e0:e1]).cuda()
         part = st["partial"][3]
-        parts[0].gspmm_weighted(st["ins"][3], wloc, out=part, reverse=True)
+        L.parts[0].gspmm_weighted(st["ins"][3], wloc, out=part, reverse=True)
         tot = part.cpu()
         dist.all_reduce(tot)
-        mine = tot.numpy()[rank * R:rank * R + hi - lo]
+        mine = tot.numpy()[rank * L.R:rank * L.R + hi - lo]
         rows = np.arange(lo, hi)
         rows = rows[np.random.default_rng(11).choice(len(rows), min(48, len(rows)), replace=False)] if len(rows) else rows
         ref, T = og.gspmm_weighted(Xh[3], wh, True, rows=rows)
