@@ -113,14 +113,21 @@ def test_gspmm_heavy_and_mega_rows(gsp):
     V, E = 4000, 600_000
     src, dst = datagen.skewed_multigraph(V, E, 3, alpha=1.6)
     G, og = graph_pair(gsp, V, src, dst)
-    assert np.diff(og.fwd_off).max() > 50_000
-    for F in (16, 64, 128):
+    deg = np.diff(og.fwd_off)
+    assert deg.max() > 50_000
+    # hub rows (degree > max(8192, E / 4096)) run as thread-block clusters of 8 CTAs
+    assert (deg > max(8192, E // 4096)).sum() >= 3
+    for F, ld in ((16, 16), (64, 64), (128, 128), (602, 604)):
         Xh = datagen.uniform(5, V, F, lo=0.0, hi=1.0)
-        X = dev(Xh)
+        X = padded(Xh, ld)
         for norm in NORMS:
             for rev in (0, 1):
                 ref, T = og.gspmm(Xh, norm, rev)
                 assert_within(G.gspmm(X, norm, reverse=rev).cpu().numpy(), ref, T, f"F{F} n{norm} r{rev}")
+        if F == 64:
+            for red in (gsp.REDUCE_MIN, gsp.REDUCE_MAX):
+                ref, _ = og.gspmm_reduce(Xh, red)
+                assert np.array_equal(G.gspmm_reduce(X, red).cpu().numpy().astype(np.float64), ref)
 
 
 @pytest.mark.parametrize("H,Fh,ld", [(1, 1, 1), (1, 3, 3), (2, 3, 6), (2, 4, 8), (8, 8, 64), (8, 8, 68),
