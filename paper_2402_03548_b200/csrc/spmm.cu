@@ -28,6 +28,10 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
     constexpr int SW = VEC * LPE * CPL;   // feature slab handled by this CTA
     constexpr bool W = MODE == kSpmmWeightedFwd || MODE == kSpmmWeightedRev;
     constexpr bool MM = MODE == kSpmmMin || MODE == kSpmmMax;   // min / max reductions (NEXT-3)
+#ifndef GSP_FF2_WIDE
+#define GSP_FF2_WIDE 1   // FFMA2 on the multi-chunk 128-bit path (Reddit F = 602: 20.0 -> 19.8 ms same box)
+#endif
+    constexpr bool FF2 = VEC >= 8 || (GSP_FF2_WIDE && VEC == 4 && CPL >= 2);
     constexpr float ID = MODE == kSpmmMin ? INFINITY : (MODE == kSpmmMax ? -INFINITY : 0.f);
     auto comb = [](float x, float y) {
         if constexpr (MODE == kSpmmMin) return fminf(x, y);
@@ -246,9 +250,9 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
 #pragma unroll
                 for (int q = 0; q < CPL; q++)
 #pragma unroll
-                    for (int t = 0; t < VEC; t += (VEC >= 8 && !MM ? 2 : 1))
+                    for (int t = 0; t < VEC; t += (FF2 && !MM ? 2 : 1))
                         if constexpr (MM) tile[u % NT][q].v[t] = comb(tile[u % NT][q].v[t], x[u][q].v[t]);
-                        else if constexpr (VEC >= 8)   // FFMA2: two features per instruction (the 256-bit
+                        else if constexpr (FF2)   // FFMA2: two features per instruction (the 256-bit
                             // path; on the 128-bit DRAM-bound path, e.g. products F = 100, it measured
                             // 8 % slower: 9.97 vs 9.18 ms same box)
                             fma2(tile[u % NT][q].v[t], tile[u % NT][q].v[t + 1], wt[u][q], wt[u][q], x[u][q].v[t],

@@ -20,6 +20,8 @@ ap.add_argument("--ops", required=True)
 ap.add_argument("--config", default="reddit")
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--reps", type=int, default=7)
+ap.add_argument("--F", type=int, default=0)
+ap.add_argument("--ld", type=int, default=0)
 args = ap.parse_args()
 vs = []
 for v in args.variants:
@@ -36,7 +38,8 @@ res = {n: {} for n, _ in vs}
 for r in range(args.rounds):
     for name, env in vs:
         out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "opbench.py"), "--config", args.config,
-                              "--ops", args.ops, "--reps", str(args.reps)], capture_output=True, text=True, env=env,
+                              "--ops", args.ops, "--reps", str(args.reps), "--F", str(args.F), "--ld", str(args.ld)],
+                             capture_output=True, text=True, env=env,
                              timeout=600)
         line = json.loads(out.stdout.strip().splitlines()[-1])
         for op, ms in line["ms"].items():
