@@ -608,9 +608,10 @@ def main_gsp(args):
     if P > 1 and G.symmetric:
         Cg = args.chunks or (4 if G.E < 128 * V else 1)
     lay_gcn = Layout(Cg)
-    lay_one = lay_gcn if Cg == 1 else Layout(1)
     fused = args.chain == "fused"
     rev_partial = P > 1 and not G.symmetric                     # directed GCN backward at N > 1
+    # the unchunked layout: only built when an op needs it (GAT ops, directed reverse)
+    lay_one = lay_gcn if (Cg == 1 or (kind == "gcn" and not rev_partial)) else Layout(1)
     # op: (name, input index, output index, exchange, layout)
     if kind == "gcn":
         op_defs = [("gspmm_fwd", 0, 0, "ag", lay_gcn),
@@ -896,7 +897,7 @@ def main_gsp(args):
     # ----------------------------------------------------------- roofline
     peak, peak_kind = load_peaks()
     time_op = make_time_op(torch, stream, flush)
-    Vloc = R if P > 1 else V
+    Vloc = (lay_one.hi - lay_one.lo) if P > 1 else V   # this rank's rows
     per_op = {}
     traffic, traffic_src = load_traffic(args.config) if P == 1 else ({}, None)
 
