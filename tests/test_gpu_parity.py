@@ -160,6 +160,28 @@ def test_weighted_heavy_rows(gsp):
         assert_within(G.gspmm_weighted(dev(Xh), dev(wh), reverse=rev).cpu().numpy(), ref, T, f"r{rev}")
 
 
+def test_weighted_8x8_every_tile_count(gsp):
+    """The H = 8 x Fh = 8 weighted kernel (wspmm8.cu) alternates register and
+    shared-memory tiles: rows of every degree 0..300 (tile counts 0..10, odd and
+    even, every ragged tail), a CTA-split hub row, and an ld = 72 table, both
+    directions (reverse through the edge ids), against oracle C5."""
+    degs = list(range(0, 301)) + [5000]
+    V = len(degs)
+    rng = np.random.default_rng(5)
+    dst = np.repeat(np.arange(V, dtype=np.int64), degs)
+    src = rng.integers(0, V, size=dst.size).astype(np.int64)
+    perm = rng.permutation(dst.size)
+    src, dst = src[perm], dst[perm]
+    G, og = graph_pair(gsp, V, src, dst)
+    Xh = datagen.uniform(11, V, 64)
+    wh = datagen.uniform(12, dst.size, 8, lo=0.0, hi=1.0)
+    for ld in (64, 72):
+        for rev in (0, 1):
+            ref, T = og.gspmm_weighted(Xh, wh, rev)
+            got = G.gspmm_weighted(padded(Xh, ld), dev(wh), reverse=rev).cpu().numpy()
+            assert_within(got, ref, T, f"ld{ld} r{rev}")
+
+
 # ------------------------------------------------------------------ gsddmm
 @pytest.mark.parametrize("H,Fh,ld", [(1, 1, 1), (1, 3, 3), (2, 3, 6), (2, 4, 8), (8, 8, 64), (8, 8, 72),
                                      (1, 32, 32), (4, 16, 64), (1, 128, 128), (2, 256, 512), (3, 5, 16)])
