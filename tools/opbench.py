@@ -28,7 +28,7 @@ E = G.E
 F = args.F or cfg.F
 ld = args.ld or max(F, cfg.ld if not args.F else F)
 H = cfg.H or 8
-Fg = H * (cfg.Fh or 8)
+Fg = H * int(os.environ.get("GSP_OPBENCH_FH", 0) or cfg.Fh or 8)   # env: other head widths (experiments)
 X = torch.from_numpy(datagen.uniform(1, V, F, ld=ld)).cuda()[:, :F]
 Z = torch.from_numpy(datagen.uniform(2, V, Fg)).cuda()
 out = torch.empty((V, F), device="cuda")
