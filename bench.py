@@ -102,6 +102,26 @@ def alg_bytes(op, V, E, F, H):
     raise KeyError(op)
 
 
+def uniq_bytes(op, V, E, F, H, edge_scales=True):
+    """B_uniq: every array the op touches counted ONCE -- the
+    gathered table once instead of once per edge; alg_bytes / uniq_bytes is the
+    reuse the L2 must supply."""
+    base = 8 * (V + 1) + 4 * E                      # offsets + column ids
+    if op in ("gspmm", "gspmm_fwd", "gspmm_rev"):
+        return base + 4 * V * F + 4 * V * F + 8 * V + (4 * E if edge_scales else 0)
+    if op == "gspmm_weighted_fwd":
+        return base + 4 * V * F + 4 * V * F + 4 * E * H
+    if op == "gspmm_weighted_rev":
+        return base + 4 * V * F + 4 * V * F + 4 * E * H + 4 * E
+    if op == "gsddmm":           # X == Y (the bench's gsddmm(Z, Z)): one table
+        return base + 4 * V * F + 4 * E * H
+    if op == "edge_softmax":
+        return 8 * (V + 1) + 4 * E * H + 4 * E * H
+    if op == "gat_forward":
+        return base + 4 * V * F + 4 * E * H + 4 * V * F
+    raise KeyError(op)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -122,6 +142,17 @@ def load_traffic(config):
         d = json.load(f)
     c = d.get(config, {})
     return {k: float(v["dram_bytes"]) for k, v in c.items()}, (c.get("gspmm_fwd") or {}).get("source")
+
+
+def load_l2_traffic(config):
+    """L2 -> L1 bytes per launch (ncu l1tex__m_xbar2l1tex_read_bytes.sum) of each op's
+    kernel from the same committed captures: what the L2 actually served."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        c = json.load(f).get(config, {})
+    return {k: float(v["l2_read_bytes"]) for k, v in c.items() if v.get("l2_read_bytes")}
 
 
 class Probe:
@@ -988,6 +1019,8 @@ def main_gsp(args):
     bytes_of = {k: alg_bytes(k, Vloc, Eloc, F, H) for k in
                 ("gspmm_fwd", "gspmm_rev", "gsddmm", "edge_softmax", "gspmm_weighted_fwd", "gspmm_weighted_rev",
                  "gat_forward")}
+    uniq_of = {k: uniq_bytes(k, Vloc, Eloc, F, H, edge_scales=G.memory()["edge_scales"] > 0) for k in bytes_of}
+    l2traffic = load_l2_traffic(args.config) if P == 1 else {}
     for k, ms in [(k, avg[k]) for k in op_names] + list(outside.items()):
         gbs = bytes_of[k] / (ms * 1e-3) / 1e9
         per_op[k] = {"ms": round(ms, 4), "GE_s": round(Eloc / (ms * 1e-3) / 1e9, 3),
@@ -998,7 +1031,9 @@ def main_gsp(args):
                      "dram_GB_s": round(traffic[k] / (ms * 1e-3) / 1e9, 1) if k in traffic else None,
                      "dram_frac_of_hbm_peak": round(traffic[k] / (ms * 1e-3) / 1e9 / peak, 4) if k in traffic else None,
                      # SURVEY §8(d) "reuse = B_alg / DRAM bytes" (> 1: the gathers are L2-served)
-                     "reuse": round(bytes_of[k] / traffic[k], 2) if traffic.get(k) else None}
+                     "reuse": round(bytes_of[k] / traffic[k], 2) if traffic.get(k) else None,
+                     "uniq_GB": round(uniq_of[k] / 1e9, 3),
+                     "ncu_l2_to_l1_GB": round(l2traffic[k] / 1e9, 3) if k in l2traffic else None}
     if P > 1:
         per_op["exchange"] = {"ms": round(avg["exchange"], 4),
                               "what": f"GCN ops {Cg} chunk(s) per all-gather; all-gathers / reduce-scatters "

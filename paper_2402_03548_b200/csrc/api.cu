@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <new>
 #include <string>
 #include <vector>
@@ -176,6 +177,41 @@ gsp_status upload_structure(gsp_graph *g, gsp::DevStructure &S, int64_t nrows, i
     return GSP_OK;
 }
 
+// Hot-row L2 policy of the scaled gSpMM (DESIGN.md §6 "Hot rows"): when the gathered
+// table is larger than L2, the rows of the highest-degree sources -- the ones gathered
+// most often -- are loaded evict_last and all others evict_first, so the streaming
+// cold rows stop pushing the reused rows out.  The BOTH norm's column scale d^-1/2 is
+// already in the kernel's registers per edge, so "degree above T" is the test
+// scale < T^-1/2: T is the degree of the k-th hottest column, k = the rows that fit in
+// ~1.3x L2 (GSP_HOT_MB overrides the budget; GSP_HOT=0 turns the policy off).  Returns
+// 0 (everything evict_last, as for L2-resident tables) when it does not apply.
+float hot_scale_for(const gsp_graph *g, int norm, int reverse, const gsp_tensor *X) {
+    static const int on = [] {
+        const char *e = getenv("GSP_HOT");
+        return e ? atoi(e) : 1;
+    }();
+    if (!on || norm != GSP_NORM_BOTH) return 0.f;
+    const std::vector<int32_t> &deg = reverse ? g->col_deg_rev : g->col_deg_fwd;
+    if (deg.empty()) return 0.f;
+    static const int64_t l2 = [] {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return int64_t(0);
+        }
+        return (int64_t)v;
+    }();
+    static const int64_t budget = [] {
+        const char *e = getenv("GSP_HOT_MB");
+        return e ? (int64_t)atoll(e) << 20 : int64_t(0);
+    }();
+    const int64_t row_bytes = X->ld * 4, table = X->rows * row_bytes;
+    if (l2 <= 0 || row_bytes <= 0 || table <= l2) return 0.f;
+    const int64_t k = std::min<int64_t>((int64_t)deg.size() - 1, (budget ? budget : l2 * 13 / 10) / row_bytes);
+    const int32_t T = std::max<int32_t>(deg[(size_t)k], 1);
+    return (float)(1.0 / std::sqrt((double)T));
+}
+
 // schedule of the edge-ID indirected reverse ops (graph.h task_id)
 const int32_t *eid_task(const gsp::DevStructure &S) { return S.task_id ? S.task_id : S.task; }
 
@@ -297,6 +333,13 @@ static gsp_status upload_full(gsp_graph *g) {
         dout.assign((size_t)h.V, 0);
         for (int32_t u : h.fwd_col) dout[u]++;
     }
+    auto sorted_desc = [](const std::vector<int64_t> &d) {
+        std::vector<int32_t> s(d.begin(), d.end());
+        std::sort(s.begin(), s.end(), std::greater<int32_t>());
+        return s;
+    };
+    g->col_deg_fwd = sorted_desc(dout);   // fwd columns are sources
+    g->col_deg_rev = sorted_desc(din);    // rev columns are destinations
     const float *inv_in, *rsq_in, *inv_out, *rsq_out;
     if ((st = make_scales(g, din, &inv_in, &rsq_in)) != GSP_OK) return st;
     if ((st = make_scales(g, dout, &inv_out, &rsq_out)) != GSP_OK) return st;
@@ -473,6 +516,7 @@ gsp_status gsp_gspmm(const gsp_graph *g, const gsp_tensor *X, int norm, gsp_tens
     a.row_scale = S.row_scale[norm]; a.col_scale = S.col_scale[norm]; a.edge_scale = S.edge_scale[norm];
     a.H = 1; a.Fh = X->cols > 0 ? X->cols : 1;
     a.light = S.nnz < 32 * S.nrows;
+    a.hot_scale = hot_scale_for(g, norm, reverse, X);
     cudaError_t e = gsp::launch_spmm(a, gsp::kSpmmScaled, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "gspmm launch");
     return GSP_OK;
@@ -961,6 +1005,8 @@ static gsp_status partition_impl(const gsp_graph *g, int nparts, int nchunks, in
             for (int64_t v = b[q]; v < b[q + 1]; v++) pmap[v] = q;
         auto padded = [&](int64_t v) { return slot(pmap[v]) * R + (v - b[pmap[v]]); };
         const int64_t NC = (int64_t)Q * R;
+        pg->col_deg_fwd = g->col_deg_fwd;   // global degrees: the scales are the full graph's
+        pg->col_deg_rev = g->col_deg_rev;
         gsp::HostGraph &lh = pg->host;
         lh.V = R;
         lh.E = off[re] - base;

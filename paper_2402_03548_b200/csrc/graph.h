@@ -91,4 +91,7 @@ struct gsp_graph {
     int64_t bytes_by[4] = {0, 0, 0, 0};
     bool edge_scales = false;
     bool edge_ids = true;      // false: GSP_BUILD_NO_EDGE_IDS (no rev_eid / lrev on the device)
+    // column degrees of the fwd / rev structure sorted descending (host): the hot-row L2
+    // policy of the scaled gSpMM on tables larger than L2 (api.cu hot_scale_for)
+    std::vector<int32_t> col_deg_fwd, col_deg_rev;
 };

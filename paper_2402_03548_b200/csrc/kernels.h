@@ -29,6 +29,7 @@ struct SpmmArgs {
     int wpol;                // L2 policy of the weight rows: 0 evict_first (streamed once), 1 evict_normal, 2 evict_last
     int light;               // mean degree < 32 (set by the caller): launch shapes that favour rows in flight
     int out_vec;             // out rows 16-B aligned (ldo % 4 == 0): vector stores, else scalar (set by launch_spmm)
+    float hot_scale;         // scaled mode: column scale below which a source row is "hot" (L2 evict_last; 0 = all)
 };
 
 enum SpmmMode { kSpmmScaled = 0, kSpmmWeightedFwd = 1, kSpmmWeightedRev = 2, kSpmmMin = 3, kSpmmMax = 4 };

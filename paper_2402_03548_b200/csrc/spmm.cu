@@ -233,9 +233,15 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
 #pragma unroll
                     for (int q = 0; q < CPL; q++) {
                         if (ok && fv[q]) {
+                            // hot-row policy (scaled mode, BOTH norm; api.cu hot_scale_for): a source
+                            // whose column scale d^-1/2 is below a.hot_scale (degree above the hot
+                            // threshold) keeps its row in L2 (evict_last), cold rows stream (evict_first)
+                            uint64_t gp_pol = pol.keep;
+                            if constexpr (MODE == kSpmmScaled && HAS_CS)
+                                if (a.hot_scale > 0.f && ww[k] >= a.hot_scale) gp_pol = pol.stream;
                             ld_keep(x[u + k][q],
                                     reinterpret_cast<const float *>(xl[q] + (uint64_t)(uint32_t)cc[k] * ldxb),
-                                    pol.keep);
+                                    gp_pol);
                         } else {
 #pragma unroll
                             for (int t = 0; t < VEC; t++) x[u + k][q].v[t] = ID;   // identity of the reduction
@@ -604,6 +610,7 @@ cudaError_t launch_spmm(const SpmmArgs &a_in, int mode, cudaStream_t s) {
     SpmmArgs a = a_in;
     a.pf = prefetch_tiles();
     a.wpol = mode == kSpmmWeightedRev ? wrev_policy() : 0;
+
     const bool wmode = mode == kSpmmWeightedFwd || mode == kSpmmWeightedRev;
     if (wmode && a.H > kHMax) return cudaErrorNotSupported;   // api.cu rejects H > 16 first
     // the gather width depends on X only; an output stride that is not a multiple of 4

@@ -47,6 +47,8 @@ for src in srcs:
         gb = float(r[col["dram__bytes_read.sum"]]) + float(r[col["dram__bytes_write.sum"]])
         cfg[op] = {"dram_bytes": gb * 1e9, "ms": float(r[col["gpu__time_duration.sum"]]),
                    "l2_hit_pct": float(r[col["lts__t_sector_hit_rate.pct"]]),
+                   "l2_read_bytes": float(r[col["l1tex__m_xbar2l1tex_read_bytes.sum"]]) * 1e9
+                   if "l1tex__m_xbar2l1tex_read_bytes.sum" in col else None,
                    "kernel": name, "source": os.path.relpath(src)}
 json.dump(d, open(out, "w"), indent=1)
 print(json.dumps(d, indent=1))
