@@ -178,7 +178,7 @@ gsp_status upload_structure(gsp_graph *g, gsp::DevStructure &S, int64_t nrows, i
 }
 
 // Hot-row L2 policy of the scaled gSpMM (DESIGN.md §6 "Hot rows"): when the gathered
-// table is larger than L2, the rows of the highest-degree sources -- the ones gathered
+// table is many times larger than L2, the rows of the highest-degree sources -- the ones gathered
 // most often -- are loaded evict_last and all others evict_first, so the streaming
 // cold rows stop pushing the reused rows out.  The BOTH norm's column scale d^-1/2 is
 // already in the kernel's registers per edge, so "degree above T" is the test
@@ -205,8 +205,11 @@ float hot_scale_for(const gsp_graph *g, int norm, int reverse, const gsp_tensor 
         const char *e = getenv("GSP_HOT_MB");
         return e ? (int64_t)atoll(e) << 20 : int64_t(0);
     }();
+    // only tables several times the L2: at 4.5x (Reddit F = 602, 561 MB) plain LRU already
+    // serves 63 % of the gathers and the hint costs 19.4 -> 29.0 ms; at 7.8x (ogbn-products,
+    // 980 MB, 9 % hits) it saves 4 %, at 160x (Kron-25) 5 %
     const int64_t row_bytes = X->ld * 4, table = X->rows * row_bytes;
-    if (l2 <= 0 || row_bytes <= 0 || table <= l2) return 0.f;
+    if (l2 <= 0 || row_bytes <= 0 || table <= 6 * l2) return 0.f;
     const int64_t k = std::min<int64_t>((int64_t)deg.size() - 1, (budget ? budget : l2 * 13 / 10) / row_bytes);
     const int32_t T = std::max<int32_t>(deg[(size_t)k], 1);
     return (float)(1.0 / std::sqrt((double)T));

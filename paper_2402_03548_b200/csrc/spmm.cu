@@ -18,7 +18,7 @@ namespace {
 // MODE kSpmmScaled      : out[r] = rs(r) * sum_j cs(col_j) * X[col_j]          (gSpMMv + norm)
 // MODE kSpmmWeightedFwd : out[r, h-block] = sum_j w[j, h] * X[col_j, h-block]   (gSpMMve)
 // MODE kSpmmWeightedRev : out[r, h-block] = sum_k w[eid_k, h] * X[col_k, ...]   (gSpMMve^T via eid)
-template <int VEC, int LPE, int CPL, int MODE, bool HAS_CS, int UOVR = 0, int MINB = 0>
+template <int VEC, int LPE, int CPL, int MODE, bool HAS_CS, int UOVR = 0, int MINB = 0, bool HOT = false>
 __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 : 2))) spmm_kernel(const SpmmArgs a) {
     constexpr int G = 32 / LPE;           // edge groups per warp
     constexpr int PER = LPE;              // edges per group per 32-edge tile
@@ -236,9 +236,10 @@ __global__ void __launch_bounds__(kThreads, (MINB ? MINB : (VEC * CPL <= 8 ? 3 :
                             // hot-row policy (scaled mode, BOTH norm; api.cu hot_scale_for): a source
                             // whose column scale d^-1/2 is below a.hot_scale (degree above the hot
                             // threshold) keeps its row in L2 (evict_last), cold rows stream (evict_first)
+                            // (a separate instantiation: the all-evict_last kernels stay as they were)
                             uint64_t gp_pol = pol.keep;
-                            if constexpr (MODE == kSpmmScaled && HAS_CS)
-                                if (a.hot_scale > 0.f && ww[k] >= a.hot_scale) gp_pol = pol.stream;
+                            if constexpr (HOT && MODE == kSpmmScaled && HAS_CS)
+                                if (ww[k] >= a.hot_scale) gp_pol = pol.stream;
                             ld_keep(x[u + k][q],
                                     reinterpret_cast<const float *>(xl[q] + (uint64_t)(uint32_t)cc[k] * ldxb),
                                     gp_pol);
@@ -499,7 +500,9 @@ template <int VEC, int LPE, int CPL, int UOVR = 0, int MINB = 0>
 cudaError_t spmm_go_v(const SpmmArgs &a, int mode, int64_t slabs, cudaStream_t s) {
     const dim3 grid = row_grid(a.nrows, a.n_heavy, slabs);
     if (mode == kSpmmScaled) {
-        if (a.col_scale || a.edge_scale) spmm_kernel<VEC, LPE, CPL, kSpmmScaled, true, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
+        if ((a.col_scale || a.edge_scale) && a.hot_scale > 0.f)
+            spmm_kernel<VEC, LPE, CPL, kSpmmScaled, true, UOVR, MINB, true><<<grid, kThreads, 0, s>>>(a);
+        else if (a.col_scale || a.edge_scale) spmm_kernel<VEC, LPE, CPL, kSpmmScaled, true, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
         else spmm_kernel<VEC, LPE, CPL, kSpmmScaled, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
     } else if (mode == kSpmmWeightedFwd) {
         spmm_kernel<VEC, LPE, CPL, kSpmmWeightedFwd, false, UOVR, MINB><<<grid, kThreads, 0, s>>>(a);
