@@ -320,3 +320,33 @@ def test_bench_nccl_path_control_flow(config, ranks, rank):
         line = json.loads(r.stdout.strip().splitlines()[-1])
         assert line["n_gpus"] == ranks and line["e2e"]["value"] > 0 and line["value"] > 0
         assert "fake" in line["per_op"]["exchange"]["what"]
+
+
+_HOT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[2])
+import datagen, paper_2402_03548_b200 as gsp
+V, E, F = 1_500_000, 15_000_000, 128             # table 768 MB > 6 x the B200's 126 MB L2
+src, dst = datagen.skewed_multigraph(V, E, 17, alpha=0.8)
+G = gsp.Graph(V, src, dst, device=0)
+X = torch.from_numpy(datagen.uniform(5, V, F)).cuda()
+outs = [G.gspmm(X, gsp.NORM_BOTH, reverse=r).cpu().numpy() for r in (0, 1)]
+np.save(sys.argv[1], np.stack(outs))
+"""
+
+
+def test_hot_row_policy_is_bitwise_neutral(tmp_path):
+    """The hot-row L2 policy (api.cu hot_scale_for: tables > 6x L2, BOTH norm) only
+    changes cache hints: gSpMM fwd / rev with it and with GSP_HOT=0 agree bit for bit.
+    (Accuracy of the hot path against the oracle: test_products_gspmm_sampled.)"""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for hot in ("1", "0"):
+        out = tmp_path / f"hot{hot}.npy"
+        env = dict(os.environ, GSP_HOT=hot)
+        subprocess.run([sys.executable, "-c", _HOT_SCRIPT, str(out), root], env=env, check=True, timeout=600)
+        res.append(np.load(out))
+    assert np.array_equal(res[0], res[1])
