@@ -191,8 +191,9 @@ float hot_scale_for(const gsp_graph *g, int norm, int reverse, const gsp_tensor 
         return e ? atoi(e) : 1;
     }();
     if (!on || norm != GSP_NORM_BOTH) return 0.f;
-    const std::vector<int32_t> &deg = reverse ? g->col_deg_rev : g->col_deg_fwd;
-    if (deg.empty()) return 0.f;
+    const auto &dp = reverse ? g->col_deg_rev : g->col_deg_fwd;
+    if (!dp || dp->empty()) return 0.f;
+    const std::vector<int32_t> &deg = *dp;
     static const int64_t l2 = [] {
         int dev = 0, v = 0;
         if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) != cudaSuccess) {
@@ -337,9 +338,9 @@ static gsp_status upload_full(gsp_graph *g) {
         for (int32_t u : h.fwd_col) dout[u]++;
     }
     auto sorted_desc = [](const std::vector<int64_t> &d) {
-        std::vector<int32_t> s(d.begin(), d.end());
-        std::sort(s.begin(), s.end(), std::greater<int32_t>());
-        return s;
+        auto s = std::make_shared<std::vector<int32_t>>(d.begin(), d.end());
+        std::sort(s->begin(), s->end(), std::greater<int32_t>());
+        return std::shared_ptr<const std::vector<int32_t>>(std::move(s));
     };
     g->col_deg_fwd = sorted_desc(dout);   // fwd columns are sources
     g->col_deg_rev = sorted_desc(din);    // rev columns are destinations

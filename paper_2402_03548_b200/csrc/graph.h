@@ -1,6 +1,7 @@
 // Internal types of libgsp (not part of the ABI; see include/gsp.h).
 #pragma once
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -93,5 +94,6 @@ struct gsp_graph {
     bool edge_ids = true;      // false: GSP_BUILD_NO_EDGE_IDS (no rev_eid / lrev on the device)
     // column degrees of the fwd / rev structure sorted descending (host): the hot-row L2
     // policy of the scaled gSpMM on tables larger than L2 (api.cu hot_scale_for)
-    std::vector<int32_t> col_deg_fwd, col_deg_rev;
+    // (shared, immutable: partitions point at their parent's)
+    std::shared_ptr<const std::vector<int32_t>> col_deg_fwd, col_deg_rev;
 };
