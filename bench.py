@@ -913,6 +913,40 @@ def main_gsp(args):
         # the metric end to end: the GCN forward layer (A3, + its all-gather at N > 1) as a
         # user runs it layer after layer -- X uploaded from pinned host memory, the layer's
         # output read back, every step
+        def link_gbs(dst, src, st_):
+            """this box's host link: GB/s of one pinned copy of the layer's table, alone"""
+            ts = []
+            for _ in range(3):
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(st_):
+                    a0.record(st_)
+                    dst.copy_(src, non_blocking=True)
+                    a1.record(st_)
+                torch.cuda.synchronize()
+                ts.append(a0.elapsed_time(a1))
+            return round(src.numel() * 4 / (min(ts) * 1e-3) / 1e9, 1)
+        link = {"h2d_GB_s": link_gbs(sets[1]["ins"][0], hin[0], h2d),
+                "d2h_GB_s": link_gbs(hin[0], sets[1]["ins"][0], d2h)}
+        # both directions at once (what the pipelined layer does every step)
+        hscratch = torch.empty_like(hin[0]).pin_memory()
+        tb = []
+        for _ in range(3):
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            h2d.wait_event(a0)
+            d2h.wait_event(a0)
+            with torch.cuda.stream(h2d):
+                sets[1]["ins"][0].copy_(hin[0], non_blocking=True)
+            with torch.cuda.stream(d2h):
+                hscratch.copy_(set0["ins"][0], non_blocking=True)
+            stream.wait_stream(h2d)
+            stream.wait_stream(d2h)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            tb.append(a0.elapsed_time(a1))
+        link["both_directions_ms"] = round(min(tb), 4)
+        del hscratch
+        hin[0].copy_(ins0[0].cpu())
         t_l, K, bi, bo = run_e2e([d for d in op_defs if d[0] == "gspmm_fwd"])
         # and the whole step the same way (all inputs up, all vertex outputs back)
         t_s, _, bis, bos = run_e2e(op_defs)
@@ -923,7 +957,11 @@ def main_gsp(args):
                "step": {"ops": op_names, "ms": round(t_s, 4), "GE_s": round(visits / (t_s * 1e-3) / 1e9, 4),
                         "h2d_bytes_per_step": int(bis), "d2h_bytes_per_step": int(bos)},
                "how": "pinned host buffers, H2D / D2H engines overlapped with the kernels and pipelined across "
-                      "steps (two device buffer sets); no L2 flush (per-step inputs exceed L2)"}
+                      "steps (two device buffer sets); no L2 flush (per-step inputs exceed L2)",
+               # the host link of this box, measured alone: the layer's e2e floor is
+               # max(kernel, bytes / link) -- box-dependent (PCIe / NUMA placement)
+               "link": link, "link_floor_ms": link["both_directions_ms"] if bi == bo else
+               round(max(bi / link["h2d_GB_s"], bo / link["d2h_GB_s"]) / 1e6, 4)}
         del sets
         torch.cuda.empty_cache()
 
