@@ -158,6 +158,10 @@ gsp_status gsp_graph_export(const gsp_graph *g, int64_t *fwd_off, int32_t *fwd_c
  *  backward, with the column-side degree applied per non-zero -- P:1536-1540.)
  * Shapes: X [ncols, F], out [nrows, F] with F = X->cols = out->cols >= 0;
  * ncols = nrows = V for a full graph (partition graphs: see gsp_graph_partition).
+ * Cache hint: with norm = BOTH and an X table larger than 6x the device's L2,
+ * rows of the highest-degree sources are gathered L2 evict_last and the rest
+ * evict_first (DESIGN.md §6 "Hot rows"; env GSP_HOT=0 disables).  Results are
+ * unaffected.
  * Errors: NULL, ARG (bad norm/reverse, host-only graph), SHAPE, ALIAS (out
  * overlaps X), NO_REVERSE, CUDA (launch failure). */
 gsp_status gsp_gspmm(const gsp_graph *g, const gsp_tensor *X, int norm, gsp_tensor *out,
